@@ -1,0 +1,133 @@
+"""CPU oracle for the in situ DataBin hot path (arXiv 2310.02926, Sec. 4.2).
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py``'s ``cpu_baseline`` / ``--impl reference`` legs may import this
+package.  The product package ``paper_2310_02926_b200`` never imports it.
+
+The arithmetic lives in ``databin_oracle.c`` (plain C, fp64, compiled with
+``-O2 -ffp-contract=off``); this module only builds it with gcc and marshals
+numpy arrays through ctypes.  See the C file's header for the passages each
+function follows.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "databin_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lock = threading.Lock()
+_lib = None
+
+CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-std=c11"]
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with gcc (no CUDA, no shared code with the product)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def _load():
+    global _lib
+    with _lock:
+        if _lib is None:
+            lib = ctypes.CDLL(build())
+            P = ctypes.POINTER
+            d_p, u64_p, i32_p = P(ctypes.c_double), P(ctypes.c_uint64), P(ctypes.c_int32)
+            dpp = P(P(ctypes.c_double))
+            lib.oracle_databin.argtypes = [
+                ctypes.c_int, i32_p, ctypes.c_int, d_p, d_p, ctypes.c_int, ctypes.c_int64,
+                dpp, ctypes.c_int, dpp, u64_p, d_p, d_p, d_p, d_p, d_p, u64_p, u64_p]
+            lib.oracle_databin.restype = ctypes.c_int
+            lib.oracle_bounds.argtypes = [ctypes.c_int, ctypes.c_int64, dpp, d_p, d_p]
+            lib.oracle_bounds.restype = ctypes.c_int
+            lib.oracle_eq1_device.argtypes = [ctypes.c_int] * 5
+            lib.oracle_eq1_device.restype = ctypes.c_int
+            _lib = lib
+    return _lib
+
+
+def _dptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def _ptr_array(cols):
+    arr = (ctypes.POINTER(ctypes.c_double) * max(1, len(cols)))()
+    for i, c in enumerate(cols):
+        arr[i] = _dptr(c)
+    return arr
+
+
+def _as_f64(cols, n=None):
+    out = [np.ascontiguousarray(c, dtype=np.float64) for c in cols]
+    for c in out:
+        if c.ndim != 1 or (n is not None and c.shape[0] != n):
+            raise ValueError("columns must be 1-D and of equal length")
+    return out
+
+
+def databin(axes, attrs, res, lo=None, hi=None, bounds_auto=False, P=1):
+    """Bin rows (axes[d][i], attrs[a][i]) onto a res[0] x ... mesh.
+
+    Returns a dict with count (u64[B]), sum/sumabs/min/max/avg (f64[A, B]),
+    n_in, n_out, lo, hi.  Bins are linearised x fastest (reading R11).
+    ``P`` > 1 runs the partition (multi-rank) mode of PAPER.md:479.
+    """
+    lib = _load()
+    ndim = len(axes)
+    if not 1 <= ndim <= 3 or len(res) != ndim:
+        raise ValueError("1..3 axes with one resolution each")
+    n = int(np.asarray(axes[0]).shape[0])
+    axes = _as_f64(axes, n)
+    attrs = _as_f64(attrs, n)
+    nattr = len(attrs)
+    resa = np.ascontiguousarray(res, dtype=np.int32)
+    B = int(np.prod(resa.astype(np.int64)))
+    loa = np.zeros(3, np.float64)
+    hia = np.zeros(3, np.float64)
+    if not bounds_auto:
+        loa[:ndim] = lo
+        hia[:ndim] = hi
+    count = np.zeros(B, np.uint64)
+    shp = (max(nattr, 1), B)
+    s, sa, mn, mx, avg = (np.zeros(shp, np.float64) for _ in range(5))
+    n_in = ctypes.c_uint64(0)
+    n_out = ctypes.c_uint64(0)
+    rc = lib.oracle_databin(
+        ndim, resa.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), int(bool(bounds_auto)),
+        _dptr(loa), _dptr(hia), int(P), n, _ptr_array(axes), nattr, _ptr_array(attrs),
+        count.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), _dptr(s), _dptr(sa),
+        _dptr(mn), _dptr(mx), _dptr(avg), ctypes.byref(n_in), ctypes.byref(n_out))
+    if rc != 0:
+        raise ValueError(f"oracle_databin failed rc={rc}")
+    k = slice(0, nattr)
+    return dict(count=count, sum=s[k], sumabs=sa[k], min=mn[k], max=mx[k], avg=avg[k],
+                n_in=int(n_in.value), n_out=int(n_out.value),
+                lo=loa[:ndim].copy(), hi=hia[:ndim].copy())
+
+
+def bounds(axes):
+    """Exact per-axis (min, max) under IEEE totalOrder, before widening."""
+    lib = _load()
+    n = int(np.asarray(axes[0]).shape[0])
+    axes = _as_f64(axes, n)
+    lo = np.zeros(3)
+    hi = np.zeros(3)
+    rc = lib.oracle_bounds(len(axes), n, _ptr_array(axes), _dptr(lo), _dptr(hi))
+    if rc != 0:
+        raise ValueError("auto bounds of an empty column")
+    return lo[:len(axes)].copy(), hi[:len(axes)].copy()
+
+
+def eq1_device(r, n_u, s, d0, n_a):
+    """Eq. (1), read as ((r mod n_u)*s + d0) mod n_a."""
+    return int(_load().oracle_eq1_device(r, n_u, s, d0, n_a))
