@@ -1,0 +1,148 @@
+// db_internal.h -- internal declarations of libdatabin (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <mutex>
+#include <string>
+
+#include "../../include/databin.h"
+
+namespace db {
+
+// ---------------------------------------------------------------- errors
+int set_error(int code, const char *fmt, ...);
+int cuda_error(cudaError_t e, const char *what);
+#define DB_CUDA(expr)                                         \
+    do {                                                      \
+        cudaError_t e_ = (expr);                              \
+        if (e_ != cudaSuccess) return ::db::cuda_error(e_, #expr); \
+    } while (0)
+
+// ---------------------------------------------------------------- allocator
+void *dev_alloc(size_t bytes, int device, cudaStream_t stream, bool async);
+void dev_free(void *p, int device, cudaStream_t stream, bool async);
+void *host_alloc(size_t bytes, bool pinned);
+void host_free(void *p, bool pinned);
+void *uva_alloc(size_t bytes);
+void uva_free(void *p);
+void count_alloc(int64_t bytes);
+void count_free(int64_t bytes);
+
+// RAII device switch
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (dev >= 0 && dev != prev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+}  // namespace db
+
+// ---------------------------------------------------------------- array handle
+struct bin_array {
+    std::atomic<int> refs{1};
+    void *ptr = nullptr;
+    int64_t n = 0;
+    int32_t dtype = BIN_F64;
+    int32_t device = -1;  // -1 host
+    bin_allocator_t alloc = BIN_ALLOC_EXTERNAL;
+    cudaStream_t stream = nullptr;
+    bin_stream_mode_t mode = BIN_SYNC;
+    bool owned = false;  // library frees ptr with `alloc`
+    void (*release)(void *, void *) = nullptr;
+    void *release_ctx = nullptr;
+    bin_array *source = nullptr;  // views keep their source alive
+    cudaEvent_t last_use = nullptr;  // last library work reading/writing this memory
+    int last_use_device = -1;
+    std::mutex mu;
+};
+
+namespace db {
+// records an event on `s` (on device `dev`) marking library work that reads `a`
+int array_mark_use(bin_array *a, cudaStream_t s, int dev);
+bool is_device_memory(const bin_array *a);
+}  // namespace db
+
+// ---------------------------------------------------------------- kernels
+namespace db {
+
+struct Geom {
+    int32_t ndim;
+    int32_t res[3];
+    int32_t bounds_auto;
+    double lo[3], hi[3];
+};
+
+// Meta block written by the finalize kernel into mapped pinned host memory.
+struct Meta {
+    int32_t status;  // 0 ok, BIN_EDEGENERATE
+    int32_t variant;
+    uint64_t n_in, n_out;
+    double lo[3], hi[3];
+    int32_t window[6];  // origin[3], extent[3]
+    int32_t done;
+    int32_t pad;
+};
+
+struct Accum {
+    unsigned long long *count;  // nbins + 2 (n_in, n_out)
+    double *sum;                // nsum * nbins
+    unsigned long long *mm;     // nmm * nbins * 2: {enc(min), ~enc(max)}
+    unsigned long long *bounds; // 2*ndim: {enc(lo_d)..., ~enc(hi_d)...}
+    int32_t *window;            // 6 ints: origin[3], extent[3]
+    uint32_t *whist;            // 4096 coarse-cell sample counts (window choice)
+    uint32_t *fxexp;            // 16: max biased exponent of each summed attribute over the sample
+    double *omin, *omax, *oavg; // outputs
+    uint64_t nbins;
+    int32_t nsum, nmm;
+    uint32_t sum_mask, mm_mask, load_mask;
+};
+
+struct Inputs {
+    const double *ax[3];
+    const double *at[BIN_MAX_ATTR];
+    int64_t n;
+    int32_t nattr;
+};
+
+struct LaunchCfg {
+    int sms;
+    int smem_optin;  // bytes per block
+};
+
+// Each returns cudaError_t of the launch.
+cudaError_t launch_init(const Accum &acc, int ndim, cudaStream_t s);
+cudaError_t launch_bounds(const Geom &g, const Inputs &in, const Accum &acc, const LaunchCfg &lc,
+                          cudaStream_t s);
+cudaError_t launch_window(const Geom &g, const Inputs &in, const Accum &acc, int wcap, cudaStream_t s);
+cudaError_t launch_bin(const Geom &g, const Inputs &in, const Accum &acc, const LaunchCfg &lc, int wcap,
+                       int smem_bytes, cudaStream_t s);
+cudaError_t launch_finalize(const Geom &g, const Accum &acc, Meta *meta_dev, int64_t n_rows_local,
+                            int variant, cudaStream_t s);
+// bytes of shared memory per window bin
+int window_bytes_per_bin(const Accum &acc);
+
+// deterministic mode (sort-based, bit-exact vs the sequential oracle)
+struct DetScratch {
+    uint32_t *keys = nullptr, *keys_alt = nullptr;   // bin index per row (or ~0 for outside)
+    uint32_t *rows = nullptr, *rows_alt = nullptr;   // row index permutation
+    uint32_t *hist = nullptr;                        // digit histograms
+    uint32_t *offsets = nullptr;                     // bin segment starts (nbins + 1)
+    int64_t cap_rows = 0;
+    int64_t cap_hist = 0;
+    uint64_t cap_bins = 0;
+    int device = -1;
+};
+cudaError_t launch_deterministic(const Geom &g, const Inputs &in, const Accum &acc, DetScratch &ds,
+                                 const LaunchCfg &lc, cudaStream_t s, int *launches);
+void free_det_scratch(DetScratch &ds);
+cudaError_t launch_rank_fold(const double *gathered, int nranks, uint64_t len, double *sum, int sms, cudaStream_t s);
+int ensure_det_scratch(DetScratch &ds, int64_t n, uint64_t nbins, int device, int sms);
+
+}  // namespace db

@@ -1,0 +1,613 @@
+// handle.cpp -- the DataBin operator instance: placement and execution
+// method (Sec. 3), input view resolution (a1), the phase
+// sequence of one execute, the NCCL cross-rank combine (a6)
+// and results.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <nccl.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <vector>
+
+#include "db_internal.h"
+
+using namespace db;
+
+namespace {
+
+enum { EV_STAGE = 0, EV_INIT0, EV_INIT1, EV_BOUNDS1, EV_WINDOW1, EV_BIN1, EV_COMBINE1, EV_FINAL1, EV_N };
+
+struct Slot {
+    Accum acc{};
+    Meta *meta_h = nullptr, *meta_d = nullptr;
+    cudaEvent_t done = nullptr, released = nullptr;
+    cudaEvent_t ev[EV_N] = {};
+    bool prof_pending = false;
+    uint64_t ticket = 0;
+    bool used = false;
+    cudaStream_t stream = nullptr;
+    int launches = 0;
+    int bin_launches = 0;
+    int variant = 0;
+    size_t dev_bytes = 0;
+};
+
+struct Stage {
+    void *p = nullptr;
+    size_t bytes = 0;
+};
+
+}  // namespace
+
+struct bin_handle {
+    bin_spec_t spec{};
+    bin_placement_t place{};
+    int rank = 0, nranks = 1;
+    int device = 0;
+    ncclComm_t comm = nullptr;
+    cudaStream_t side = nullptr;
+    Slot slot[2];
+    uint64_t next_ticket = 1;
+    Stage stage[2][BIN_MAX_DIM + BIN_MAX_ATTR];
+    cudaEvent_t producer_ev[BIN_MAX_DIM + BIN_MAX_ATTR] = {};
+    LaunchCfg lc{};
+    int wcap = 0, smem_bytes = 0;
+    uint64_t nbins = 1;
+    int nsum = 0, nmm = 0;
+    uint32_t sum_mask = 0, mm_mask = 0, load_mask = 0;
+    bool prof = false;
+    bin_profile_t pacc{};
+    cudaStream_t last = nullptr;
+    DetScratch det;
+    double *gather = nullptr;  // deterministic multi-rank: nranks x nsum x nbins partial sums
+    size_t gather_bytes = 0;
+    bool finalized = false;
+};
+
+static int nccl_error(ncclResult_t r, const char *what) {
+    return set_error(BIN_ENCCL, "%s: %s", what, ncclGetErrorString(r));
+}
+
+static void free_slot(bin_handle *h, Slot &s) {
+    DeviceGuard g(h->device);
+    if (s.acc.count) { cudaFree(s.acc.count); count_free((int64_t)s.dev_bytes); }
+    s.acc = Accum{};
+    if (s.meta_h) { cudaFreeHost(s.meta_h); count_free((int64_t)sizeof(Meta)); }
+    s.meta_h = s.meta_d = nullptr;
+    if (s.done) cudaEventDestroy(s.done);
+    if (s.released) cudaEventDestroy(s.released);
+    for (auto &e : s.ev)
+        if (e) cudaEventDestroy(e), e = nullptr;
+    s.done = s.released = nullptr;
+}
+
+static int alloc_slot(bin_handle *h, Slot &s) {
+    const uint64_t B = h->nbins;
+    // one device allocation, carved (all pieces 16-byte aligned)
+    auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    size_t o_count = 0;
+    size_t o_sum = o_count + al((B + 2) * 8);
+    size_t o_mm = o_sum + al(B * 8 * h->nsum);
+    size_t o_bounds = o_mm + al(B * 16 * h->nmm);
+    size_t o_window = o_bounds + al(6 * 8);
+    size_t o_whist = o_window + al(8 * 4);
+    size_t o_fxexp = o_whist + al(4096 * 4);
+    size_t o_omin = o_fxexp + al(16 * 4);
+    size_t o_omax = o_omin + al(B * 8 * h->nmm);
+    size_t o_oavg = o_omax + al(B * 8 * h->nmm);
+    size_t total = o_oavg + al(B * 8 * h->nsum);
+    unsigned char *base = nullptr;
+    cudaError_t e = cudaMalloc(&base, total);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return set_error(BIN_ENOMEM, "bin_init: %zu bytes of bin arrays on device %d", total, h->device);
+    }
+    count_alloc((int64_t)total);
+    s.dev_bytes = total;
+    s.acc.count = (unsigned long long *)(base + o_count);
+    s.acc.sum = (double *)(base + o_sum);
+    s.acc.mm = (unsigned long long *)(base + o_mm);
+    s.acc.bounds = (unsigned long long *)(base + o_bounds);
+    s.acc.window = (int32_t *)(base + o_window);
+    s.acc.whist = (uint32_t *)(base + o_whist);
+    s.acc.fxexp = (uint32_t *)(base + o_fxexp);
+    s.acc.omin = (double *)(base + o_omin);
+    s.acc.omax = (double *)(base + o_omax);
+    s.acc.oavg = (double *)(base + o_oavg);
+    s.acc.nbins = B;
+    s.acc.nsum = h->nsum;
+    s.acc.nmm = h->nmm;
+    s.acc.sum_mask = h->sum_mask;
+    s.acc.mm_mask = h->mm_mask;
+    s.acc.load_mask = h->load_mask;
+    DB_CUDA(cudaHostAlloc((void **)&s.meta_h, sizeof(Meta), cudaHostAllocMapped | cudaHostAllocPortable));
+    count_alloc((int64_t)sizeof(Meta));
+    memset(s.meta_h, 0, sizeof(Meta));
+    DB_CUDA(cudaHostGetDevicePointer((void **)&s.meta_d, s.meta_h, 0));
+    DB_CUDA(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
+    DB_CUDA(cudaEventCreateWithFlags(&s.released, cudaEventDisableTiming));
+    for (auto &ev : s.ev) DB_CUDA(cudaEventCreate(&ev));
+    return BIN_OK;
+}
+
+static int validate_spec(const bin_spec_t *sp, uint64_t *nbins) {
+    if (sp->ndim < 1 || sp->ndim > BIN_MAX_DIM) return set_error(BIN_ENOTSUP, "ndim %d not in 1..3", sp->ndim);
+    if (sp->nattr < 0 || sp->nattr > BIN_MAX_ATTR) return set_error(BIN_ENOTSUP, "nattr %d not in 0..16", sp->nattr);
+    uint64_t B = 1;
+    for (int d = 0; d < sp->ndim; ++d) {
+        if (sp->res[d] < 1) return set_error(BIN_EINVAL, "res[%d] = %d < 1", d, sp->res[d]);
+        B *= (uint64_t)sp->res[d];
+        if (B >= (1ull << 32)) return set_error(BIN_EINVAL, "prod(res) >= 2^32");
+        if (!sp->bounds_auto) {
+            if (!(sp->lo[d] < sp->hi[d]) || !isfinite(sp->lo[d]) || !isfinite(sp->hi[d]))
+                return set_error(BIN_EINVAL, "axis %d: need finite lo < hi (got %g, %g)", d, sp->lo[d], sp->hi[d]);
+            if (!isfinite((double)sp->res[d] / (sp->hi[d] - sp->lo[d])) || sp->hi[d] - sp->lo[d] == INFINITY)
+                return set_error(BIN_EINVAL, "axis %d: hi - lo overflows", d);
+        }
+    }
+    for (int a = 0; a < sp->nattr; ++a)
+        if (sp->ops[a] & ~(uint32_t)(BIN_OP_SUM | BIN_OP_MIN | BIN_OP_MAX | BIN_OP_AVG))
+            return set_error(BIN_EINVAL, "ops[%d] = 0x%x has unknown bits", a, sp->ops[a]);
+    *nbins = B;
+    return BIN_OK;
+}
+
+extern "C" {
+
+void bin_placement_default(bin_placement_t *p) {
+    if (!p) return;
+    p->device_id = BIN_DEVICE_AUTO;
+    p->device_start = 0;
+    p->device_stride = 1;
+    p->devices_to_use = 0;
+    p->exec = BIN_EXEC_SYNC;
+    p->async_snapshot = 1;
+}
+
+int bin_resolve_device(const bin_placement_t *p, int32_t rank, int32_t n_avail, int32_t *device) {
+    if (!p || !device) return set_error(BIN_EINVAL, "bin_resolve_device: NULL argument");
+    if (n_avail < 1) return set_error(BIN_EDEVICE, "no devices available (n_a = %d)", n_avail);
+    if (p->device_id == BIN_DEVICE_HOST)
+        return set_error(BIN_ENOTSUP, "host placement (device_id = -1): this library has no CPU path");
+    if (p->device_id >= 0) {
+        if (p->device_id >= n_avail) return set_error(BIN_EDEVICE, "device_id %d >= %d devices", p->device_id, n_avail);
+        *device = p->device_id;
+        return BIN_OK;
+    }
+    if (p->device_id != BIN_DEVICE_AUTO) return set_error(BIN_EDEVICE, "device_id %d", p->device_id);
+    if (rank < 0) return set_error(BIN_EINVAL, "rank %d < 0", rank);
+    if (p->device_stride < 1) return set_error(BIN_EINVAL, "device_stride %d < 1", p->device_stride);
+    if (p->device_start < 0) return set_error(BIN_EINVAL, "device_start %d < 0", p->device_start);
+    int n_u = p->devices_to_use > 0 ? p->devices_to_use : n_avail;  // default n_u = n_a
+    // Eq. (1): d = ((r mod n_u) * s + d_0) mod n_a  (reading R14)
+    long long d = ((long long)(rank % n_u) * p->device_stride + p->device_start) % n_avail;
+    *device = (int32_t)d;
+    return BIN_OK;
+}
+
+int bin_nccl_unique_id(void *out128) {
+    if (!out128) return set_error(BIN_EINVAL, "bin_nccl_unique_id: NULL");
+    ncclUniqueId id;
+    ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) return nccl_error(r, "ncclGetUniqueId");
+    static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+    memcpy(out128, &id, 128);
+    return BIN_OK;
+}
+
+int bin_init(const bin_spec_t *spec, const bin_placement_t *place, const bin_comm_t *comm, bin_handle_t **out) {
+    if (!spec || !out) return set_error(BIN_EINVAL, "bin_init: NULL spec/out");
+    *out = nullptr;
+    uint64_t B = 0;
+    int rc = validate_spec(spec, &B);
+    if (rc) return rc;
+    bin_placement_t pl;
+    if (place) pl = *place;
+    else bin_placement_default(&pl);
+    if (pl.exec < BIN_EXEC_SYNC || pl.exec > BIN_EXEC_PEER) return set_error(BIN_EINVAL, "exec %d", pl.exec);
+    int rank = comm ? comm->rank : 0, nranks = comm ? comm->nranks : 1;
+    if (nranks < 1 || rank < 0 || rank >= nranks) return set_error(BIN_EINVAL, "rank %d of %d", rank, nranks);
+    if (nranks > 1 && (!comm || !comm->nccl_unique_id))
+        return set_error(BIN_EINVAL, "nranks > 1 needs an NCCL unique id");
+    int n_a = 0;
+    cudaError_t ce = cudaGetDeviceCount(&n_a);
+    if (ce != cudaSuccess) {
+        cudaGetLastError();
+        if (pl.device_id == BIN_DEVICE_HOST) return bin_resolve_device(&pl, rank, 1, &n_a);
+        return set_error(BIN_EDEVICE, "no CUDA device: %s", cudaGetErrorString(ce));
+    }
+    int dev = 0;
+    rc = bin_resolve_device(&pl, rank, n_a, &dev);
+    if (rc) return rc;
+
+    bin_handle *h = new bin_handle;
+    h->spec = *spec;
+    h->place = pl;
+    h->rank = rank;
+    h->nranks = nranks;
+    h->device = dev;
+    h->nbins = B;
+    for (int a = 0; a < spec->nattr; ++a) {
+        uint32_t o = spec->ops[a];
+        if (o & (BIN_OP_SUM | BIN_OP_AVG)) h->sum_mask |= 1u << a;
+        if (o & (BIN_OP_MIN | BIN_OP_MAX)) h->mm_mask |= 1u << a;
+    }
+    h->load_mask = h->sum_mask | h->mm_mask;
+    h->nsum = __builtin_popcount(h->sum_mask);
+    h->nmm = __builtin_popcount(h->mm_mask);
+    DeviceGuard g(dev);
+    auto fail = [&](int code) {
+        bin_finalize(h);
+        return code;
+    };
+    if ((ce = cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking)) != cudaSuccess)
+        return fail(cuda_error(ce, "cudaStreamCreate"));
+    cudaDeviceGetAttribute(&h->lc.sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&h->lc.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    int bpb = 4 + 12 * h->nsum + 16 * h->nmm;  // window_bytes_per_bin()
+    h->wcap = h->lc.smem_optin / bpb;
+    h->smem_bytes = (int)((uint64_t)h->wcap >= B ? B * bpb : (uint64_t)h->wcap * bpb);
+    h->smem_bytes = (h->smem_bytes + 15) & ~15;
+    for (auto &s : h->slot)
+        if ((rc = alloc_slot(h, s))) return fail(rc);
+    for (auto &e : h->producer_ev)
+        if ((ce = cudaEventCreateWithFlags(&e, cudaEventDisableTiming)) != cudaSuccess)
+            return fail(cuda_error(ce, "cudaEventCreate"));
+    if (nranks > 1 && spec->deterministic && h->nsum) {
+        h->gather_bytes = (size_t)nranks * h->nsum * B * 8;
+        h->gather = (double *)dev_alloc(h->gather_bytes, dev, nullptr, false);
+        if (!h->gather) return fail(set_error(BIN_ENOMEM, "deterministic gather buffer"));
+    }
+    if (nranks > 1) {
+        ncclUniqueId id;
+        memcpy(&id, comm->nccl_unique_id, sizeof id);
+        ncclResult_t r = ncclCommInitRank(&h->comm, nranks, id, rank);
+        if (r != ncclSuccess) {
+            h->comm = nullptr;
+            return fail(nccl_error(r, "ncclCommInitRank"));
+        }
+    }
+    *out = h;
+    return BIN_OK;
+}
+
+static void accumulate_profile(bin_handle *h, Slot &S);
+
+static int stage_buffer(bin_handle *h, int sl, int col, size_t bytes, void **p) {
+    Stage &st = h->stage[sl][col];
+    if (st.bytes < bytes) {
+        if (st.p) {
+            cudaFree(st.p);
+            count_free((int64_t)st.bytes);
+        }
+        st.p = nullptr;
+        st.bytes = 0;
+        st.p = dev_alloc(bytes, h->device, nullptr, false);
+        if (!st.p) return set_error(BIN_ENOMEM, "staging buffer of %zu bytes", bytes);
+        st.bytes = bytes;
+    }
+    *p = st.p;
+    return BIN_OK;
+}
+
+int bin_execute(bin_handle_t *h, bin_array_t *const *axes, int32_t naxes, bin_array_t *const *attrs,
+                int32_t nattr, uint64_t *ticket) {
+    if (!h || h->finalized) return set_error(BIN_ESTATE, "bin_execute: handle is NULL or finalized");
+    if (naxes != h->spec.ndim) return set_error(BIN_ESHAPE, "%d axis columns for a %dD mesh", naxes, h->spec.ndim);
+    if (nattr != h->spec.nattr) return set_error(BIN_ESHAPE, "%d attribute columns, spec has %d", nattr, h->spec.nattr);
+    bin_array *cols[BIN_MAX_DIM + BIN_MAX_ATTR];
+    int ncols = naxes + nattr;
+    for (int i = 0; i < ncols; ++i) {
+        cols[i] = i < naxes ? axes[i] : attrs[i - naxes];
+        if (!cols[i]) return set_error(BIN_EINVAL, "column %d is NULL", i);
+        if (cols[i]->dtype != BIN_F64) return set_error(BIN_EDTYPE, "column %d is not BIN_F64", i);
+        if (cols[i]->n != cols[0]->n)
+            return set_error(BIN_ESHAPE, "column %d has %lld rows, column 0 has %lld", i, (long long)cols[i]->n,
+                             (long long)cols[0]->n);
+    }
+    const int64_t n = cols[0]->n;
+    DeviceGuard g(h->device);
+    const uint64_t t = h->next_ticket++;
+    const int sl = (int)(t & 1);
+    Slot &S = h->slot[sl];
+
+    // ---- work stream (execution method)
+    cudaStream_t s = h->side;
+    if (h->place.exec == BIN_EXEC_SYNC && is_device_memory(cols[0]) && cols[0]->device == h->device)
+        s = cols[0]->stream;  // lockstep: ordered on the producer's stream
+    if (S.used && S.prof_pending) {  // keep per-phase times of every execute while profiling
+        DB_CUDA(cudaEventSynchronize(S.done));
+        accumulate_profile(h, S);
+    }
+    if (S.used && S.stream != s) DB_CUDA(cudaStreamWaitEvent(s, S.done, 0));
+    S.ticket = t;
+    S.used = true;
+    S.stream = s;
+    S.launches = 0;
+    S.bin_launches = 0;
+    h->last = s;
+    if (h->prof) DB_CUDA(cudaEventRecord(S.ev[EV_STAGE], s));
+
+    // ---- a1: resolve input views on the analysis device
+    Inputs in{};
+    in.n = n;
+    in.nattr = nattr;
+    bool staged_any = false;
+    for (int i = 0; i < ncols; ++i) {
+        bin_array *a = cols[i];
+        bool uva = a->alloc == BIN_ALLOC_CUDA_UVA;
+        bool local = uva || (is_device_memory(a) && a->device == h->device);
+        bool snapshot = h->place.exec == BIN_EXEC_ASYNC && h->place.async_snapshot;
+        const double *p = (const double *)a->ptr;
+        // order after the producer's pending work on its own stream
+        if (a->stream != s && (a->device >= 0 || a->alloc == BIN_ALLOC_HOST_PINNED)) {
+            int pd = a->device >= 0 ? a->device : h->device;
+            {
+                DeviceGuard g2(pd);
+                cudaEvent_t ev = h->producer_ev[i];
+                if (pd != h->device) {
+                    // events are per device: use a temporary on the producer's device
+                    cudaEvent_t tmp;
+                    DB_CUDA(cudaEventCreateWithFlags(&tmp, cudaEventDisableTiming));
+                    DB_CUDA(cudaEventRecord(tmp, a->stream));
+                    DeviceGuard g3(h->device);
+                    DB_CUDA(cudaStreamWaitEvent(s, tmp, 0));
+                    cudaEventDestroy(tmp);
+                } else {
+                    DB_CUDA(cudaEventRecord(ev, a->stream));
+                    DB_CUDA(cudaStreamWaitEvent(s, ev, 0));
+                }
+            }
+        }
+        if (n > 0 && (!local || snapshot)) {
+            void *dst = nullptr;
+            int rc = stage_buffer(h, sl, i, (size_t)n * 8, &dst);
+            if (rc) return rc;
+            if (a->device == -1 || a->alloc == BIN_ALLOC_HOST || a->alloc == BIN_ALLOC_HOST_PINNED)
+                DB_CUDA(cudaMemcpyAsync(dst, a->ptr, (size_t)n * 8, cudaMemcpyHostToDevice, s));
+            else if (a->device != h->device && !uva)
+                DB_CUDA(cudaMemcpyPeerAsync(dst, h->device, a->ptr, a->device, (size_t)n * 8, s));
+            else
+                DB_CUDA(cudaMemcpyAsync(dst, a->ptr, (size_t)n * 8, cudaMemcpyDeviceToDevice, s));
+            p = (const double *)dst;
+            staged_any = true;
+        }
+        if (i < naxes) in.ax[i] = p;
+        else in.at[i - naxes] = p;
+    }
+    if (staged_any) DB_CUDA(cudaEventRecord(S.released, s));  // inputs copied: producer may overwrite
+
+    Geom geom{};
+    geom.ndim = h->spec.ndim;
+    geom.bounds_auto = h->spec.bounds_auto;
+    for (int d = 0; d < 3; ++d) {
+        geom.res[d] = d < geom.ndim ? h->spec.res[d] : 1;
+        geom.lo[d] = d < geom.ndim ? h->spec.lo[d] : 0.0;
+        geom.hi[d] = d < geom.ndim ? h->spec.hi[d] : 1.0;
+    }
+    cudaError_t e;
+    auto rec = [&](int k) -> int {
+        if (h->prof) DB_CUDA(cudaEventRecord(S.ev[k], s));
+        return BIN_OK;
+    };
+    int rc;
+    if ((rc = rec(EV_INIT0))) return rc;
+    // ---- a3: accumulator identities
+    if ((e = launch_init(S.acc, geom.ndim, s)) != cudaSuccess) return cuda_error(e, "init kernel");
+    S.launches++;
+    if ((rc = rec(EV_INIT1))) return rc;
+    // ---- a2: automatic bounds (+ cross-rank Min, reading R3)
+    if (geom.bounds_auto) {
+        if ((e = launch_bounds(geom, in, S.acc, h->lc, s)) != cudaSuccess) return cuda_error(e, "bounds kernel");
+        if (n > 0) S.launches++;
+        if (h->comm) {
+            ncclResult_t r = ncclAllReduce(S.acc.bounds, S.acc.bounds, 2 * geom.ndim, ncclUint64, ncclMin, h->comm, s);
+            if (r != ncclSuccess) return nccl_error(r, "ncclAllReduce(bounds)");
+        }
+    }
+    if ((rc = rec(EV_BOUNDS1))) return rc;
+    int variant;
+    if (h->spec.deterministic) {
+        if ((rc = rec(EV_WINDOW1))) return rc;
+        int launches = 0;
+        if ((rc = ensure_det_scratch(h->det, n, h->nbins, h->device, h->lc.sms))) return rc;
+        if ((e = launch_deterministic(geom, in, S.acc, h->det, h->lc, s, &launches)) != cudaSuccess)
+            return cuda_error(e, "deterministic binning");
+        S.launches += launches;
+        S.bin_launches += 1;
+        variant = 3;
+    } else {
+        // ---- hot-window choice, then a4 + a5
+        if ((e = launch_window(geom, in, S.acc, h->wcap, s)) != cudaSuccess) return cuda_error(e, "window kernel");
+        S.launches += 2;
+        if ((rc = rec(EV_WINDOW1))) return rc;
+        if (n / h->lc.sms >= (int64_t)0xffffffffLL)
+            return set_error(BIN_EINVAL, "%lld rows per call exceed the per-CTA u32 window counters", (long long)n);
+        if ((e = launch_bin(geom, in, S.acc, h->lc, h->wcap, h->smem_bytes, s)) != cudaSuccess)
+            return cuda_error(e, "bin kernel");
+        if (n > 0) S.launches++, S.bin_launches++;
+        variant = (uint64_t)h->wcap >= h->nbins ? 2 : 1;
+    }
+    if ((rc = rec(EV_BIN1))) return rc;
+    // ---- a6: cross-rank combine over NVLink (one NCCL group)
+    if (h->comm) {
+        const uint64_t B = h->nbins;
+        ncclResult_t r = ncclGroupStart();
+        if (r == ncclSuccess) r = ncclAllReduce(S.acc.count, S.acc.count, B + 2, ncclUint64, ncclSum, h->comm, s);
+        if (r == ncclSuccess && h->nsum && !h->gather)
+            r = ncclAllReduce(S.acc.sum, S.acc.sum, B * h->nsum, ncclFloat64, ncclSum, h->comm, s);
+        if (r == ncclSuccess && h->nsum && h->gather)  // deterministic: gather partials, fold in rank order
+            r = ncclAllGather(S.acc.sum, h->gather, B * h->nsum, ncclFloat64, h->comm, s);
+        if (r == ncclSuccess && h->nmm)
+            r = ncclAllReduce(S.acc.mm, S.acc.mm, B * h->nmm * 2, ncclUint64, ncclMin, h->comm, s);
+        ncclResult_t r2 = ncclGroupEnd();
+        if (r != ncclSuccess) return nccl_error(r, "ncclAllReduce(bins)");
+        if (r2 != ncclSuccess) return nccl_error(r2, "ncclGroupEnd");
+        if (h->gather) {
+            if ((e = launch_rank_fold(h->gather, h->nranks, B * h->nsum, S.acc.sum, h->lc.sms, s)) != cudaSuccess)
+                return cuda_error(e, "rank-ordered fold");
+            S.launches++;
+        }
+    }
+    if ((rc = rec(EV_COMBINE1))) return rc;
+    // ---- a7: finalize
+    S.meta_h->done = 0;
+    if ((e = launch_finalize(geom, S.acc, S.meta_d, n, variant, s)) != cudaSuccess) return cuda_error(e, "finalize kernel");
+    S.launches++;
+    S.variant = variant;
+    if ((rc = rec(EV_FINAL1))) return rc;
+    DB_CUDA(cudaEventRecord(S.done, s));
+    if (!staged_any) DB_CUDA(cudaEventRecord(S.released, s));
+    S.prof_pending = h->prof;
+    for (int i = 0; i < ncols; ++i)
+        if ((rc = array_mark_use(cols[i], s, h->device))) return rc;
+    if (ticket) *ticket = t;
+    if (h->place.exec == BIN_EXEC_SYNC && cols[0]->mode == BIN_SYNC) {
+        e = cudaEventSynchronize(S.done);
+        if (e != cudaSuccess) return cuda_error(e, "bin_execute (lockstep) synchronize");
+    }
+    return BIN_OK;
+}
+
+static Slot *find_slot(bin_handle *h, uint64_t t) {
+    Slot &S = h->slot[t & 1];
+    return (S.used && S.ticket == t) ? &S : nullptr;
+}
+
+int bin_inputs_released(bin_handle_t *h, uint64_t ticket, bin_event_t *ev) {
+    if (!h || !ev) return set_error(BIN_EINVAL, "bin_inputs_released: NULL argument");
+    Slot *S = find_slot(h, ticket);
+    if (!S) return set_error(BIN_ESTATE, "unknown or recycled ticket %llu", (unsigned long long)ticket);
+    *ev = (bin_event_t)S->released;
+    return BIN_OK;
+}
+
+static void accumulate_profile(bin_handle *h, Slot &S) {
+    if (!S.prof_pending) return;
+    S.prof_pending = false;
+    float ms[EV_N] = {};
+    for (int k = 1; k < EV_N; ++k) cudaEventElapsedTime(&ms[k], S.ev[k - 1], S.ev[k]);
+    cudaGetLastError();
+    bin_profile_t &p = h->pacc;
+    p.ms_stage += ms[EV_INIT0];
+    p.ms_init += ms[EV_INIT1];
+    p.ms_bounds += ms[EV_BOUNDS1];
+    p.ms_window += ms[EV_WINDOW1];
+    p.ms_bin += ms[EV_BIN1];
+    p.ms_combine += ms[EV_COMBINE1];
+    p.ms_finalize += ms[EV_FINAL1];
+    p.executes += 1;
+    p.kernel_launches += S.launches;
+    p.bin_launches += S.bin_launches;
+    p.variant = S.variant;
+    for (int d = 0; d < 3; ++d) p.window[d] = S.meta_h->window[3 + d];
+}
+
+int bin_wait(bin_handle_t *h, uint64_t ticket) {
+    if (!h || h->finalized) return set_error(BIN_ESTATE, "bin_wait: handle is NULL or finalized");
+    Slot *S = find_slot(h, ticket);
+    if (!S) return set_error(BIN_ESTATE, "unknown or recycled ticket %llu", (unsigned long long)ticket);
+    DeviceGuard g(h->device);
+    cudaError_t e = cudaEventSynchronize(S->done);
+    if (e != cudaSuccess) return cuda_error(e, "bin_wait");
+    accumulate_profile(h, *S);
+    if (S->meta_h->status == BIN_EDEGENERATE)
+        return set_error(BIN_EDEGENERATE, "auto bounds: no finite rows in total, or an infinite/unrecoverable axis");
+    return BIN_OK;
+}
+
+int bin_result(bin_handle_t *h, uint64_t ticket, bin_result_t *out) {
+    if (!out) return set_error(BIN_EINVAL, "bin_result: NULL out");
+    int rc = bin_wait(h, ticket);
+    if (rc) return rc;
+    Slot &S = *find_slot(h, ticket);
+    memset(out, 0, sizeof *out);
+    const uint64_t B = h->nbins;
+    out->count = (const uint64_t *)S.acc.count;
+    for (int a = 0; a < h->spec.nattr; ++a) {
+        uint32_t o = h->spec.ops[a];
+        if ((h->sum_mask >> a) & 1u) {
+            int slot = __builtin_popcount(h->sum_mask & ((1u << a) - 1u));
+            if (o & BIN_OP_SUM) out->sum[a] = S.acc.sum + (uint64_t)slot * B;
+            if (o & BIN_OP_AVG) out->avg[a] = S.acc.oavg + (uint64_t)slot * B;
+        }
+        if ((h->mm_mask >> a) & 1u) {
+            int slot = __builtin_popcount(h->mm_mask & ((1u << a) - 1u));
+            if (o & BIN_OP_MIN) out->min[a] = S.acc.omin + (uint64_t)slot * B;
+            if (o & BIN_OP_MAX) out->max[a] = S.acc.omax + (uint64_t)slot * B;
+        }
+    }
+    out->nbins = B;
+    out->n_in = S.meta_h->n_in;
+    out->n_out = S.meta_h->n_out;
+    out->device = h->device;
+    for (int d = 0; d < 3; ++d) {
+        out->lo[d] = d < h->spec.ndim ? S.meta_h->lo[d] : 0.0;
+        out->hi[d] = d < h->spec.ndim ? S.meta_h->hi[d] : 0.0;
+    }
+    return BIN_OK;
+}
+
+int bin_stream(bin_handle_t *h, bin_stream_t *stream) {
+    if (!h || !stream) return set_error(BIN_EINVAL, "bin_stream: NULL argument");
+    *stream = (bin_stream_t)(h->last ? h->last : h->side);
+    return BIN_OK;
+}
+
+int bin_profile_enable(bin_handle_t *h, int32_t on) {
+    if (!h) return set_error(BIN_EINVAL, "bin_profile_enable: NULL handle");
+    h->prof = on != 0;
+    memset(&h->pacc, 0, sizeof h->pacc);
+    return BIN_OK;
+}
+
+int bin_profile_read(bin_handle_t *h, bin_profile_t *out) {
+    if (!h || !out) return set_error(BIN_EINVAL, "bin_profile_read: NULL argument");
+    DeviceGuard g(h->device);
+    for (auto &S : h->slot)
+        if (S.prof_pending && cudaEventQuery(S.done) == cudaSuccess) accumulate_profile(h, S);
+    *out = h->pacc;
+    return BIN_OK;
+}
+
+int bin_finalize(bin_handle_t *h) {
+    if (!h) return BIN_OK;
+    int rc = BIN_OK;
+    {
+        DeviceGuard g(h->device);
+        for (auto &S : h->slot)
+            if (S.done) {
+                cudaError_t e = cudaEventSynchronize(S.done);
+                if (e != cudaSuccess && rc == BIN_OK) rc = cuda_error(e, "bin_finalize");
+            }
+        if (h->side) cudaStreamSynchronize(h->side);
+        if (h->comm) {
+            ncclCommDestroy(h->comm);
+            h->comm = nullptr;
+        }
+        for (auto &S : h->slot) free_slot(h, S);
+        for (auto &row : h->stage)
+            for (auto &st : row)
+                if (st.p) {
+                    cudaFree(st.p);
+                    count_free((int64_t)st.bytes);
+                    st.p = nullptr;
+                }
+        for (auto &e : h->producer_ev)
+            if (e) cudaEventDestroy(e), e = nullptr;
+        free_det_scratch(h->det);
+        if (h->gather) {
+            cudaFree(h->gather);
+            count_free((int64_t)h->gather_bytes);
+            h->gather = nullptr;
+        }
+        if (h->side) cudaStreamDestroy(h->side);
+        h->side = nullptr;
+    }
+    h->finalized = true;
+    delete h;
+    return rc;
+}
+
+}  // extern "C"
