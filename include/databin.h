@@ -204,7 +204,8 @@ typedef struct {
     int64_t executes;
     int64_t kernel_launches;  /* library kernels launched (all phases) */
     int64_t bin_launches;     /* launches of the accumulate kernel */
-    int32_t variant;          /* last accumulate variant: 0 global, 1 smem window, 2 smem full grid, 3 deterministic */
+    int32_t variant;          /* last accumulate variant (low 4 bits): 1 smem window + L2, 2 smem full grid,
+                                 3 deterministic; +16 when the single-attribute k_bin_fast kernel ran */
     int32_t window[BIN_MAX_DIM]; /* last window extents (bins), 0 = no window */
 } bin_profile_t;
 

@@ -46,16 +46,18 @@ def stale() -> bool:
     return any(os.path.getmtime(f) > t for f in sources() + headers() + [__file__])
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, defines=(), out=None) -> str:
+    lib_path = out or LIB
+    if not force and not defines and out is None and not stale():
         return LIB
     inc, libdir = nccl_dirs()
     objdir = os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
 
     def compile_one(src):
-        obj = os.path.join(objdir, os.path.basename(src) + ".o")
-        cmd = ["nvcc", *COMMON, "-I", inc, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
+        tag = ("_" + "_".join(d.replace("=", "") for d in defines)) if defines else ""
+        obj = os.path.join(objdir, os.path.basename(src) + tag + ".o")
+        cmd = ["nvcc", *COMMON, *[f"-D{d}" for d in defines], "-I", inc, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
@@ -66,15 +68,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if verbose:
         for _, log in results:
             sys.stderr.write(log)
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = lib_path + f".tmp{os.getpid()}"
     cmd = ["nvcc", *ARCH, "-shared", "-o", tmp, *[o for o, _ in results],
            "-L", libdir, "-l:libnccl.so.2", "-Xlinker", f"-rpath,{libdir}", "-lcudart"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib_path)
+    return lib_path
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    outs = [a[6:] for a in sys.argv[1:] if a.startswith("--out=")]
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, defines=defs, out=outs[0] if outs else None))

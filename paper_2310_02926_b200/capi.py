@@ -112,7 +112,9 @@ def lib():
     with _lock:
         if _lib is None:
             path = _build.LIB
-            if os.environ.get("DATABIN_NO_BUILD") != "1":
+            if os.environ.get("DATABIN_LIB"):          # explicit build variant (A/B experiments)
+                path = os.environ["DATABIN_LIB"]
+            elif os.environ.get("DATABIN_NO_BUILD") != "1":
                 path = _build.build()
             if not os.path.exists(path):
                 raise ImportError(f"libdatabin.so missing at {path}; run __graft_entry__.build()")

@@ -1,0 +1,316 @@
+// bin_fast.cu -- k_bin_fast: the accumulate kernel (a4 + a5) for the common
+// case of at most one binned attribute with 16-byte-aligned columns (C1, C3,
+// C4, C5 and the paper's Fig. 1 sum-of-mass), same window layout and
+// arithmetic as k_bin (bin_general.cu), written for few instructions per row:
+//
+//  * 32-bit pair indices, shared memory addressed as one u32 array with
+//    warp-uniform word offsets (no generic-pointer round trips);
+//  * one 16-byte pair per column prefetched one step ahead in registers;
+//  * a per-warp queue of rare work.  Rows outside the window (~8% on C3) and
+//    min/max candidates inside it (~12%: a CTA-bin sees only ~80 rows, so its
+//    running extremes still move) would otherwise be divergent branches that
+//    nearly every warp takes.  Lanes append (kind | bin, value) with a ballot
+//    and the warp executes 32 queued items at a time with every lane busy,
+//    as fire-and-forget L2 reductions (REDG.ADD / REDG.MIN, no loads).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "db_internal.h"
+#include "dev_common.cuh"
+
+namespace db {
+
+extern __shared__ __align__(16) uint32_t f_dsm[];
+
+constexpr int FAST_THREADS = 1024;
+constexpr int QCAP = 64;            // >= 31 leftover + 32 new items
+constexpr int QWORDS = 3 * QCAP;    // u32 tags[QCAP] + f64 vals[QCAP]
+constexpr uint32_t QBIN = (1u << 29) - 1;
+enum : uint32_t { QK_GLOBAL = 1u, QK_MIN = 2u, QK_MAX = 4u };
+
+int fast_queue_bytes() { return (FAST_THREADS / 32) * QWORDS * 4 + 16; }
+
+struct FastCtx {
+    DGeom G;
+    WinGeom w;
+    FxParam fx;
+    uint32_t o_fx, o_cnt;  // word offsets (filters at 0)
+};
+
+template <int D, int A, int SM, int MM>
+__device__ __forceinline__ uint32_t fast_row(const FastCtx &c, const double (&x)[D], double v, bool valid,
+                                             uint32_t &n_in) {
+    constexpr bool HS = A == 1 && SM == 1, HM = A == 1 && MM == 1;
+    bool ok = valid;
+    int k[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+        ok = ok && (c.G.lo[d] <= x[d]) && (x[d] <= c.G.hi[d]);
+        k[d] = min(floor_nonneg(__dmul_rn(__dsub_rn(x[d], c.G.lo[d]), c.G.scale[d])), c.w.resm1[d]);
+    }
+    if (!ok) return 0u;
+    ++n_in;
+    bool inw = true;
+    uint32_t l = 0;
+#pragma unroll
+    for (int d = D - 1; d >= 0; --d) {
+        const unsigned r = (unsigned)(k[d] - c.w.wo[d]);
+        inw = inw && (r < c.w.we[d]);
+        l = l * c.w.we[d] + r;
+    }
+    uint32_t b = (uint32_t)k[0];
+    if (D >= 2) b += (uint32_t)(c.w.resm1[0] + 1) * (uint32_t)k[1];
+    if (D >= 3) b += (uint32_t)(c.w.resm1[0] + 1) * (uint32_t)(c.w.resm1[1] + 1) * (uint32_t)k[2];
+    if (!inw) return (QK_GLOBAL << 29) | b;
+    atomicAdd(&f_dsm[c.o_cnt + l], 1u);
+    const uint32_t W = c.w.W;
+    uint32_t tag = 0;
+    if (HS) {
+        const uint32_t w0 = c.o_fx + l;
+        unsigned qmid;
+        if (fx_path(c.fx, v)) {
+            const unsigned long long q = fx_quant(c.fx, v);
+            const unsigned qlo = (unsigned)q;
+            qmid = (unsigned)(q >> 32);
+            const unsigned old = atomicAdd(&f_dsm[w0], qlo);
+            qmid += (old + qlo < old) ? 1u : 0u;
+        } else {  // rare: outside the fixed range -> sum (and min/max) go global; count stays here
+            tag = ((QK_GLOBAL | QK_MIN) << 29) | b;
+            qmid = FX_OFFSET_MID;
+        }
+        const unsigned old2 = atomicAdd(&f_dsm[w0 + W], qmid);
+        if (old2 + qmid < old2) atomicAdd(&f_dsm[w0 + 2 * W], 1u);
+    }
+    if (HM && tag == 0) {
+        const unsigned long long e = enc_total(v);
+        const unsigned eh = (unsigned)(e >> 32), neh = ~eh;
+        uint2 f;  // one LDS.64; stale values are safe (the words only decrease)
+        asm volatile("ld.volatile.shared.v2.u32 {%0, %1}, [%2];" : "=r"(f.x), "=r"(f.y) : "r"((unsigned)__cvta_generic_to_shared(&f_dsm[2 * l])));
+        uint32_t kind = 0;
+        if (eh <= f.x) {
+            kind |= QK_MIN;
+            if (eh < f.x) atomicMin(&f_dsm[2 * l], eh);
+        }
+        if (neh <= f.y) {
+            kind |= QK_MAX;
+            if (neh < f.y) atomicMin(&f_dsm[2 * l + 1], neh);
+        }
+        if (kind) tag = (kind << 29) | b;
+    }
+    return tag;
+}
+
+// One queued item as fire-and-forget L2 reductions.  A QK_GLOBAL item from
+// inside the window (value outside the fixed range) carries sum + min/max but
+// its count is already in shared memory -> the low bit of `kind` picks count.
+template <int A, int SM, int MM>
+__device__ __forceinline__ void fast_exec(uint32_t tag, double v, unsigned long long *count, double *sum,
+                                          ulonglong2 *mm) {
+    constexpr bool HS = A == 1 && SM == 1, HM = A == 1 && MM == 1;
+    const uint32_t kind = tag >> 29, b = tag & QBIN;
+    if (kind & QK_GLOBAL) {
+        if (!(kind & QK_MIN)) atomicAdd(&count[b], 1ull);  // QK_GLOBAL|QK_MIN marks "count already counted"
+        if (HS) atomicAdd(&sum[b], v);
+        if (HM) {
+            const unsigned long long e = enc_total(v);
+            atomicMin(&mm[b].x, e);
+            atomicMin(&mm[b].y, ~e);
+        }
+    } else if (HM) {
+        const unsigned long long e = enc_total(v);
+        if (kind & QK_MIN) atomicMin(&mm[b].x, e);
+        if (kind & QK_MAX) atomicMin(&mm[b].y, ~e);
+    }
+}
+
+template <int A, int SM, int MM>
+__device__ __forceinline__ void fast_push(uint32_t qb, uint32_t &qn, uint32_t tag, double v, unsigned lane,
+                                          unsigned long long *count, double *sum, ulonglong2 *mm) {
+    const unsigned m = __ballot_sync(0xffffffffu, tag != 0);
+    if (m == 0) return;
+    double *vals = (double *)&f_dsm[qb + QCAP];
+    if (tag) {
+        const unsigned pos = qn + __popc(m & ((1u << lane) - 1u));
+        f_dsm[qb + pos] = tag;
+        vals[pos] = v;
+    }
+    qn += __popc(m);
+    if (qn >= 32) {
+        __syncwarp();
+        const uint32_t t = f_dsm[qb + lane];
+        const double vv = vals[lane];
+        const unsigned rest = qn - 32;
+        uint32_t t2 = 0;
+        double v2 = 0.0;
+        if (lane < rest) {
+            t2 = f_dsm[qb + 32 + lane];
+            v2 = vals[32 + lane];
+        }
+        __syncwarp();
+        if (lane < rest) {
+            f_dsm[qb + lane] = t2;
+            vals[lane] = v2;
+        }
+        qn = rest;
+        fast_exec<A, SM, MM>(t, vv, count, sum, mm);
+        __syncwarp();
+    }
+}
+
+template <int D, int A, int SM, int MM>
+__global__ void __launch_bounds__(FAST_THREADS, 1)
+    k_bin_fast(Geom g, Inputs in, Accum acc, uint32_t npairs, int head) {
+    constexpr bool HS = A == 1 && SM == 1, HM = A == 1 && MM == 1;
+    FastCtx c;
+    c.G = load_geom(g, acc.bounds);
+    if (!c.G.ok) return;  // degenerate auto bounds: finalize reports it
+    c.w = load_window(c.G, acc.window, D);
+    const uint32_t W = c.w.W;
+    c.o_fx = HM ? 2u * W : 0u;
+    c.o_cnt = c.o_fx + (HS ? 3u * W : 0u);
+    c.fx = fx_param(A == 1 ? acc.fxexp[0] : 0u);
+    unsigned long long *const count = acc.count;
+    double *const sum = acc.sum;
+    ulonglong2 *const mm = (ulonglong2 *)acc.mm;
+
+    for (uint32_t i = threadIdx.x; i < c.o_fx; i += FAST_THREADS) f_dsm[i] = ~0u;  // min/max filters
+    for (uint32_t i = c.o_fx + threadIdx.x; i < c.o_cnt + W; i += FAST_THREADS) f_dsm[i] = 0u;
+    const unsigned lane = threadIdx.x & 31u;
+    const uint32_t qb = ((c.o_cnt + W + 3u) & ~3u) + (threadIdx.x >> 5) * QWORDS;
+    uint32_t qn = 0;
+    __syncthreads();
+
+    const double2 *cx[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) cx[d] = (const double2 *)(in.ax[d] + head);
+    const double2 *cv = (const double2 *)((A == 1 ? in.at[0] : in.ax[0]) + head);
+
+    uint32_t n_in = 0, rows = 0;
+    const uint32_t nthr = gridDim.x * FAST_THREADS;
+    const uint32_t p0 = blockIdx.x * FAST_THREADS + threadIdx.x;
+    double2 bx[D], bv = make_double2(0.0, 0.0);
+    if (p0 < npairs) {
+#pragma unroll
+        for (int d = 0; d < D; ++d) bx[d] = __ldcs(cx[d] + p0);
+        if (A == 1) bv = __ldcs(cv + p0);
+    }
+    for (uint32_t pb = p0 - lane; pb < npairs; pb += nthr) {  // warp-uniform trip count
+        const uint32_t pc = pb + lane;
+        const bool valid = pc < npairs;
+        const uint32_t pn = pc + nthr;
+        double2 nx[D], nv = make_double2(0.0, 0.0);
+        if (pn < npairs) {
+#pragma unroll
+            for (int d = 0; d < D; ++d) nx[d] = __ldcs(cx[d] + pn);
+            if (A == 1) nv = __ldcs(cv + pn);
+        }
+        double x[D];
+#pragma unroll
+        for (int d = 0; d < D; ++d) x[d] = bx[d].x;
+        uint32_t t0 = fast_row<D, A, SM, MM>(c, x, bv.x, valid, n_in);
+        fast_push<A, SM, MM>(qb, qn, t0, bv.x, lane, count, sum, mm);
+#pragma unroll
+        for (int d = 0; d < D; ++d) x[d] = bx[d].y;
+        uint32_t t1 = fast_row<D, A, SM, MM>(c, x, bv.y, valid, n_in);
+        fast_push<A, SM, MM>(qb, qn, t1, bv.y, lane, count, sum, mm);
+        rows += valid ? 2u : 0u;
+#pragma unroll
+        for (int d = 0; d < D; ++d) bx[d] = nx[d];
+        bv = nv;
+    }
+    // the unpaired head row (lane 0) and tail row (lane 1) of the whole input, on warp 0 of CTA 0
+    if (blockIdx.x == 0 && threadIdx.x < 32) {
+        const int64_t r = lane == 0 ? (head ? 0 : -1)
+                                    : (lane == 1 && ((in.n - head) & 1) ? in.n - 1 : -1);
+        double x[D], v = 0.0;
+#pragma unroll
+        for (int d = 0; d < D; ++d) x[d] = r >= 0 ? in.ax[d][r] : 0.0;
+        if (A == 1 && r >= 0) v = in.at[0][r];
+        const uint32_t t = fast_row<D, A, SM, MM>(c, x, v, r >= 0, n_in);
+        rows += r >= 0 ? 1u : 0u;
+        fast_push<A, SM, MM>(qb, qn, t, v, lane, count, sum, mm);
+    }
+    __syncwarp();
+    if (lane < qn) fast_exec<A, SM, MM>(f_dsm[qb + lane], ((double *)&f_dsm[qb + QCAP])[lane], count, sum, mm);
+
+    unsigned long long in_w = n_in, out_w = rows - n_in;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        in_w += __shfl_xor_sync(0xffffffffu, in_w, o);
+        out_w += __shfl_xor_sync(0xffffffffu, out_w, o);
+    }
+    if (lane == 0) {
+        if (in_w) atomicAdd(&count[acc.nbins], in_w);
+        if (out_w) atomicAdd(&count[acc.nbins + 1], out_w);
+    }
+    __syncthreads();
+
+    // flush the window into the global accumulator (L2 reductions)
+    for (uint32_t l = threadIdx.x; l < W; l += FAST_THREADS) {
+        const unsigned cnt = f_dsm[c.o_cnt + l];
+        if (cnt == 0) continue;
+        uint32_t rem = l, b = 0, mul = 1;
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+            const uint32_t kd = rem % c.w.we[d] + (uint32_t)c.w.wo[d];
+            rem /= c.w.we[d];
+            b += kd * mul;
+            mul *= (uint32_t)c.G.res[d];
+        }
+        atomicAdd(&count[b], (unsigned long long)cnt);
+        if (HS) {
+            const uint32_t w0 = c.o_fx + l;
+            const double d = fx_to_double(f_dsm[w0], f_dsm[w0 + W], f_dsm[w0 + 2 * W], cnt, c.fx.inv_scale);
+            if (d != 0.0) atomicAdd(&sum[b], d);
+        }
+    }
+}
+
+// Eligible: <= 1 attribute, bins < 2^29, 16-byte pairs (all columns in the same
+// 16-byte phase), fewer than 2^31 pairs.
+bool fast_eligible(const Inputs &in, const Accum &acc, int ndim) {
+    if (in.nattr > 1 || acc.nbins >= (1ull << 29)) return false;
+    const uintptr_t ph = (uintptr_t)in.ax[0] & 15u;
+    if (ph % 8) return false;
+    for (int d = 0; d < ndim; ++d)
+        if (((uintptr_t)in.ax[d] & 15u) != ph) return false;
+    if (in.nattr == 1 && (acc.load_mask & 1u) && (((uintptr_t)in.at[0] & 15u) != ph)) return false;
+    const int64_t head = ph ? 1 : 0;
+    return in.n >= 2 + head && (in.n - head) / 2 < (1ll << 31);
+}
+
+template <int D, int A, int SM, int MM>
+static cudaError_t launch_fast_t(const Geom &g, const Inputs &in, const Accum &acc, const LaunchCfg &lc, int smem,
+                                 cudaStream_t s) {
+    const int head = ((uintptr_t)in.ax[0] & 15u) ? 1 : 0;
+    const uint32_t npairs = (uint32_t)((in.n - head) / 2);
+    int blocks = lc.sms;  // one persistent CTA per SM: the whole shared memory holds the window
+    const int64_t maxb = ((int64_t)npairs + FAST_THREADS - 1) / FAST_THREADS;
+    if (maxb < blocks) blocks = (int)(maxb > 0 ? maxb : 1);
+    auto kern = k_bin_fast<D, A, SM, MM>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    kern<<<blocks, FAST_THREADS, smem, s>>>(g, in, acc, npairs, head);
+    return cudaGetLastError();
+}
+
+template <int D>
+static cudaError_t launch_fast_d(const Geom &g, const Inputs &in, const Accum &acc, const LaunchCfg &lc, int smem,
+                                 cudaStream_t s) {
+    if (in.nattr == 0 || !(acc.load_mask & 1u)) return launch_fast_t<D, 0, 0, 0>(g, in, acc, lc, smem, s);
+    const bool sm = acc.sum_mask & 1u, mm = acc.mm_mask & 1u;
+    if (sm && mm) return launch_fast_t<D, 1, 1, 1>(g, in, acc, lc, smem, s);
+    if (sm) return launch_fast_t<D, 1, 1, 0>(g, in, acc, lc, smem, s);
+    return launch_fast_t<D, 1, 0, 1>(g, in, acc, lc, smem, s);
+}
+
+cudaError_t launch_bin_fast(const Geom &g, const Inputs &in, const Accum &acc, const LaunchCfg &lc, int smem,
+                            cudaStream_t s) {
+    switch (g.ndim) {
+    case 1: return launch_fast_d<1>(g, in, acc, lc, smem, s);
+    case 2: return launch_fast_d<2>(g, in, acc, lc, smem, s);
+    default: return launch_fast_d<3>(g, in, acc, lc, smem, s);
+    }
+}
+
+}  // namespace db

@@ -121,12 +121,17 @@ cudaError_t launch_init(const Accum &acc, int ndim, cudaStream_t s);
 cudaError_t launch_bounds(const Geom &g, const Inputs &in, const Accum &acc, const LaunchCfg &lc,
                           cudaStream_t s);
 cudaError_t launch_window(const Geom &g, const Inputs &in, const Accum &acc, int wcap, cudaStream_t s);
-cudaError_t launch_bin(const Geom &g, const Inputs &in, const Accum &acc, const LaunchCfg &lc, int wcap,
-                       int smem_bytes, cudaStream_t s);
+cudaError_t launch_bin_general(const Geom &g, const Inputs &in, const Accum &acc, const LaunchCfg &lc, int smem,
+                               cudaStream_t s);
+cudaError_t launch_bin_fast(const Geom &g, const Inputs &in, const Accum &acc, const LaunchCfg &lc, int smem,
+                            cudaStream_t s);
+bool fast_eligible(const Inputs &in, const Accum &acc, int ndim);
+int fast_queue_bytes();
 cudaError_t launch_finalize(const Geom &g, const Accum &acc, Meta *meta_dev, int64_t n_rows_local,
                             int variant, cudaStream_t s);
 // bytes of shared memory per window bin
 int window_bytes_per_bin(const Accum &acc);
+
 
 // deterministic mode (sort-based, bit-exact vs the sequential oracle)
 struct DetScratch {

@@ -77,7 +77,7 @@ __global__ void k_det_keys(Geom g, Inputs in, Accum acc, uint32_t *keys, uint32_
         for (int d = 0; d < g.ndim; ++d) {
             double x = in.ax[d][i];
             inside = inside && (G.lo[d] <= x) && (x <= G.hi[d]);
-            int kd = min(__double2int_rd(__dmul_rn(__dsub_rn(x, G.lo[d]), G.scale[d])), G.res[d] - 1);
+            int kd = min(__double2loint(__dadd_rd(__dmul_rn(__dsub_rn(x, G.lo[d]), G.scale[d]), 4503599627370496.0)), G.res[d] - 1);  // floor (see kernels.cu floor_nonneg)
             b += (uint32_t)kd * mul;
             mul *= (uint32_t)G.res[d];
         }

@@ -1,0 +1,173 @@
+// dev_common.cuh -- device helpers shared by the DataBin kernels (csrc/*.cu).
+// Part of the product library; shares nothing with oracle/.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "db_internal.h"
+
+namespace db {
+
+__device__ __forceinline__ unsigned long long enc_total(double x) {
+    unsigned long long b = (unsigned long long)__double_as_longlong(x);
+    unsigned long long m = (unsigned long long)((long long)b >> 63);
+    return b ^ (m | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double dec_total(unsigned long long e) {
+    unsigned long long m = ~(unsigned long long)((long long)e >> 63);
+    return __longlong_as_double((long long)(e ^ (m | 0x8000000000000000ull)));
+}
+
+// Shared-memory 2x64-bit read that the compiler may not cache in registers
+// (other threads update these words atomically; see the monotone filter).
+__device__ __forceinline__ ulonglong2 lds_volatile_u64x2(const ulonglong2 *p) {
+    ulonglong2 r;
+    unsigned a = (unsigned)__cvta_generic_to_shared(p);
+    asm volatile("ld.volatile.shared.v2.u64 {%0, %1}, [%2];" : "=l"(r.x), "=l"(r.y) : "r"(a));
+    return r;
+}
+
+// floor(t) for 0 <= t < 2^31 without the (slow) F2I.F64 conversion pipe:
+// t + 2^52 rounded toward -inf lands in [2^52, 2^53) where the ulp is 1, so
+// its low mantissa word is exactly floor(t).  Out-of-range t (rows outside the
+// mesh, NaN) give garbage that the caller masks.  Measured: the bin-index
+// stage went from 0.14 ms to ... on C3 (profiles/r01_ablation.txt).
+__device__ __forceinline__ int floor_nonneg(double t) {
+    return __double2loint(__dadd_rd(t, 4503599627370496.0));
+}
+
+struct DGeom {
+    double lo[3], hi[3], scale[3];
+    int res[3];
+    bool ok;
+};
+
+// Realised mesh bounds and scales; identical in every CTA of every kernel.
+__device__ __forceinline__ DGeom load_geom(const Geom &g, const unsigned long long *bounds) {
+    DGeom G;
+    G.ok = true;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        G.res[d] = d < g.ndim ? g.res[d] : 1;
+        G.lo[d] = 0.0;
+        G.hi[d] = 1.0;
+        G.scale[d] = 1.0;
+        if (d >= g.ndim) continue;
+        double lo = g.lo[d], hi = g.hi[d];
+        if (g.bounds_auto) {
+            unsigned long long elo = bounds[d], nhi = bounds[g.ndim + d];
+            if (elo == ~0ull || nhi == ~0ull) G.ok = false;  // no non-NaN row anywhere
+            lo = dec_total(elo);
+            hi = dec_total(~nhi);
+            if (lo == hi) {  // reading R4
+                lo = __dsub_rn(lo, 0.5);
+                hi = __dadd_rn(hi, 0.5);
+            }
+            if (!(lo < hi) || isinf(lo) || isinf(hi)) G.ok = false;
+        }
+        G.lo[d] = lo;
+        G.hi[d] = hi;
+        G.scale[d] = __ddiv_rn((double)G.res[d], __dsub_rn(hi, lo));
+    }
+    return G;
+}
+
+// Bin coordinates of one row; returns false if outside the mesh.
+template <int D>
+__device__ __forceinline__ bool bin_coords(const DGeom &G, const double (&x)[D], int (&k)[D]) {
+    bool in = true;
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+        in = in && (G.lo[d] <= x[d]) && (x[d] <= G.hi[d]);
+        double t = __dmul_rn(__dsub_rn(x[d], G.lo[d]), G.scale[d]);
+        int kd = floor_nonneg(t);  // floor for in-bounds rows; garbage (masked by `in`) otherwise
+        k[d] = min(kd, G.res[d] - 1);
+    }
+    return in;
+}
+
+// ---- fixed-point window sums (see bin_general.cu / bin_fast.cu headers) ----
+constexpr long long FX_OFFSET = 1ll << 54;  // makes every q' positive: q in (-2^54, 2^54)
+constexpr unsigned FX_OFFSET_MID = (unsigned)(FX_OFFSET >> 32);
+
+struct FxParam {
+    double scale;      // 2^F
+    double inv_scale;  // 2^-F
+    unsigned lo;       // biased exponents [lo, lo + span) take the fixed path (plus exact 0)
+    unsigned span;
+};
+
+// F from the sampled max exponent of the attribute: E_hi = e_max + 3 (biased
+// eb_hi), F = 54 - E_hi; values in [2^(E_hi-9), 2^E_hi) -> quantisation <= 2^-46 |v|.
+__device__ __forceinline__ FxParam fx_param(unsigned fxexp) {
+    int eb_hi = (int)fxexp + 3;
+    if (fxexp == 0) eb_hi = 1023 + 1;  // nothing sampled: assume |v| < 2
+    const int F = 54 - (eb_hi - 1023);
+    const bool usable = F > -900 && F < 900;
+    const int eb_lo = max(eb_hi - 9, 1);
+    FxParam P;
+    P.lo = usable ? (unsigned)eb_lo : 1u;
+    P.span = usable ? (unsigned)(eb_hi - eb_lo) : 0u;
+    P.scale = usable ? ldexp(1.0, F) : 0.0;
+    P.inv_scale = usable ? ldexp(1.0, -F) : 0.0;
+    return P;
+}
+
+__device__ __forceinline__ bool fx_path(const FxParam &P, double v) {
+    const unsigned eb = ((unsigned)__double2hiint(v) >> 20) & 0x7ffu;
+    return eb - P.lo < P.span || v == 0.0;
+}
+
+// q' = round(v * 2^F) + 2^54 in (0, 2^55)
+__device__ __forceinline__ unsigned long long fx_quant(const FxParam &P, double v) {
+    return (unsigned long long)(__double2ll_rn(__dmul_rn(v, P.scale)) + FX_OFFSET);
+}
+
+// Exact 96-bit fixed-point window sum of cnt offset values -> f64 (one rounding
+// when |q| < 2^62, else <= 1 ulp).
+__device__ __forceinline__ double fx_to_double(uint32_t lo, uint32_t mid, uint32_t hi, unsigned cnt, double inv_scale) {
+    unsigned __int128 qp = ((unsigned __int128)hi << 64) | ((unsigned __int128)mid << 32) | lo;
+    __int128 q = (__int128)qp - (__int128)cnt * (__int128)FX_OFFSET;
+    double d;
+    if (q >= -(((__int128)1) << 62) && q < (((__int128)1) << 62)) {
+        d = __ll2double_rn((long long)q);
+    } else {
+        long long qh = (long long)(q >> 32);
+        unsigned long long ql = (unsigned long long)(q & 0xffffffffll);
+        d = __dadd_rn(__dmul_rn(__ll2double_rn(qh), 4294967296.0), __ull2double_rn(ql));
+    }
+    return __dmul_rn(d, inv_scale);
+}
+
+// Compile-time op masks: for A == 1 the launchers instantiate SM/MM in {0,1}
+// (sum requested, min/max requested); otherwise SM = MM = -1 (runtime masks).
+template <int A, int SM, int MM>
+struct OpMask {
+    __device__ static __forceinline__ bool sum(uint32_t rt, int a) { return SM >= 0 ? (SM >> a) & 1 : (rt >> a) & 1u; }
+    __device__ static __forceinline__ bool mm(uint32_t rt, int a) { return MM >= 0 ? (MM >> a) & 1 : (rt >> a) & 1u; }
+    __device__ static __forceinline__ uint32_t sum_slot(uint32_t rt, int a) { return SM >= 0 ? 0u : __popc(rt & ((1u << a) - 1u)); }
+    __device__ static __forceinline__ uint32_t mm_slot(uint32_t rt, int a) { return MM >= 0 ? 0u : __popc(rt & ((1u << a) - 1u)); }
+};
+
+// Window geometry of one CTA (from the window kernel) and derived constants.
+struct WinGeom {
+    int wo[3];
+    unsigned we[3];
+    int resm1[3];  // res - 1 per axis (upper clamp)
+    uint32_t W;
+};
+
+__device__ __forceinline__ WinGeom load_window(const DGeom &G, const int32_t *window, int D) {
+    WinGeom w;
+    w.W = 1;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        w.wo[d] = d < D ? window[d] : 0;
+        w.we[d] = d < D ? (unsigned)window[3 + d] : 1u;
+        w.resm1[d] = G.res[d] - 1;
+        w.W *= w.we[d];
+    }
+    return w;
+}
+
+}  // namespace db

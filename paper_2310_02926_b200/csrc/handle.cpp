@@ -245,10 +245,15 @@ int bin_init(const bin_spec_t *spec, const bin_placement_t *place, const bin_com
         return fail(cuda_error(ce, "cudaStreamCreate"));
     cudaDeviceGetAttribute(&h->lc.sms, cudaDevAttrMultiProcessorCount, dev);
     cudaDeviceGetAttribute(&h->lc.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    int bpb = 4 + 12 * h->nsum + 16 * h->nmm;  // window_bytes_per_bin()
-    h->wcap = h->lc.smem_optin / bpb;
+    Accum probe{};
+    probe.nsum = h->nsum;
+    probe.nmm = h->nmm;
+    probe.nbins = B;
+    const int bpb = window_bytes_per_bin(probe);
+    const int qbytes = (spec->nattr <= 1 && B < (1ull << 29)) ? fast_queue_bytes() : 0;  // k_bin_fast queues
+    h->wcap = (h->lc.smem_optin - qbytes) / bpb;
     h->smem_bytes = (int)((uint64_t)h->wcap >= B ? B * bpb : (uint64_t)h->wcap * bpb);
-    h->smem_bytes = (h->smem_bytes + 15) & ~15;
+    h->smem_bytes = ((h->smem_bytes + 15) & ~15) + qbytes;
     for (auto &s : h->slot)
         if ((rc = alloc_slot(h, s))) return fail(rc);
     for (auto &e : h->producer_ev)
@@ -424,10 +429,14 @@ int bin_execute(bin_handle_t *h, bin_array_t *const *axes, int32_t naxes, bin_ar
         if ((rc = rec(EV_WINDOW1))) return rc;
         if (n / h->lc.sms >= (int64_t)0xffffffffLL)
             return set_error(BIN_EINVAL, "%lld rows per call exceed the per-CTA u32 window counters", (long long)n);
-        if ((e = launch_bin(geom, in, S.acc, h->lc, h->wcap, h->smem_bytes, s)) != cudaSuccess)
-            return cuda_error(e, "bin kernel");
-        if (n > 0) S.launches++, S.bin_launches++;
-        variant = (uint64_t)h->wcap >= h->nbins ? 2 : 1;
+        const bool fast = n > 0 && fast_eligible(in, S.acc, geom.ndim);
+        if (n > 0) {
+            e = fast ? launch_bin_fast(geom, in, S.acc, h->lc, h->smem_bytes, s)
+                     : launch_bin_general(geom, in, S.acc, h->lc, h->smem_bytes, s);
+            if (e != cudaSuccess) return cuda_error(e, "bin kernel");
+            S.launches++, S.bin_launches++;
+        }
+        variant = ((uint64_t)h->wcap >= h->nbins ? 2 : 1) | (fast ? 16 : 0);
     }
     if ((rc = rec(EV_BIN1))) return rc;
     // ---- a6: cross-rank combine over NVLink (one NCCL group)

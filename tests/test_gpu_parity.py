@@ -175,7 +175,7 @@ def test_3d_global_path_and_window(db):
     both(db, axes, attrs, [64, 64, 64], [-1] * 3, [1] * 3, det_too=True)
     axes = [rng.standard_normal(n) * 0.1 for _ in range(3)]       # clustered: window catches most rows
     out, _ = both(db, axes, attrs, [128, 128, 128], [-1] * 3, [1] * 3, det_too=False)
-    assert out["profile"].variant == 1
+    assert out["profile"].variant & 15 == 1
 
 
 def test_zero_rows_and_degenerate_bounds(db):
@@ -213,7 +213,7 @@ def test_c3_full_100M_plummer_512x512(db):
     w = synth.CONFIGS["c3"]
     axes, attrs = workload_inputs(w)
     out, ref = both(db, axes, attrs, w.res, w.lo, w.hi, det_too=True)
-    assert out["profile"].variant == 1                      # the bench's launch configuration
+    assert out["profile"].variant == 1 | 16                 # window + k_bin_fast: the bench's launch configuration
     tot = float(np.sum(attrs[0]))
     inside_mass = float(np.sum(out["sum"][0]))
     assert 0 < out["n_out"] < w.n // 100                    # ~0.1% outside the +-16 a box
