@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(FAST_THREADS, 1)
     k_bin_fast(Geom g, Inputs in, Accum acc, uint32_t npairs, int head) {
     constexpr bool HS = A == 1 && SM == 1, HM = A == 1 && MM == 1;
     FastCtx c;
-    c.G = load_geom(g, acc.bounds);
+    c.G = load_geom<D>(g, acc.bounds);
     if (!c.G.ok) return;  // degenerate auto bounds: finalize reports it
     c.w = load_window(c.G, acc.window, D);
     const uint32_t W = c.w.W;
@@ -174,9 +174,10 @@ __global__ void __launch_bounds__(FAST_THREADS, 1)
     ulonglong2 *const mm = (ulonglong2 *)acc.mm;
 
     for (uint32_t i = threadIdx.x; i < c.o_fx; i += FAST_THREADS) f_dsm[i] = ~0u;  // min/max filters
-    for (uint32_t i = c.o_fx + threadIdx.x; i < c.o_cnt + W; i += FAST_THREADS) f_dsm[i] = 0u;
+    const uint32_t o_end = c.o_cnt + W;
+    for (uint32_t i = c.o_fx + threadIdx.x; i < o_end; i += FAST_THREADS) f_dsm[i] = 0u;
     const unsigned lane = threadIdx.x & 31u;
-    const uint32_t qb = ((c.o_cnt + W + 3u) & ~3u) + (threadIdx.x >> 5) * QWORDS;
+    const uint32_t qb = ((o_end + 3u) & ~3u) + (threadIdx.x >> 5) * QWORDS;
     uint32_t qn = 0;
     __syncthreads();
 
@@ -247,7 +248,7 @@ __global__ void __launch_bounds__(FAST_THREADS, 1)
 
     // flush the window into the global accumulator (L2 reductions)
     for (uint32_t l = threadIdx.x; l < W; l += FAST_THREADS) {
-        const unsigned cnt = f_dsm[c.o_cnt + l];
+        const unsigned long long cnt = f_dsm[c.o_cnt + l];
         if (cnt == 0) continue;
         uint32_t rem = l, b = 0, mul = 1;
 #pragma unroll
@@ -257,7 +258,7 @@ __global__ void __launch_bounds__(FAST_THREADS, 1)
             b += kd * mul;
             mul *= (uint32_t)c.G.res[d];
         }
-        atomicAdd(&count[b], (unsigned long long)cnt);
+        atomicAdd(&count[b], cnt);
         if (HS) {
             const uint32_t w0 = c.o_fx + l;
             const double d = fx_to_double(f_dsm[w0], f_dsm[w0 + W], f_dsm[w0 + 2 * W], cnt, c.fx.inv_scale);

@@ -139,7 +139,7 @@ template <int D, int A, bool VEC>
 __global__ void __launch_bounds__(GenThreads<A>::value, 1)
     k_bin(Geom g, Inputs in, Accum acc, int64_t head) {
     GenCtx c;
-    c.G = load_geom(g, acc.bounds);
+    c.G = load_geom<D>(g, acc.bounds);
     if (!c.G.ok) return;  // degenerate auto bounds: finalize reports it
     c.w = load_window(c.G, acc.window, D);
     const uint32_t W = c.w.W;
@@ -158,7 +158,8 @@ __global__ void __launch_bounds__(GenThreads<A>::value, 1)
     const uint32_t load_mask = acc.load_mask;
 
     for (uint32_t i = threadIdx.x; i < c.o_fx; i += blockDim.x) g_dsm[i] = ~0u;  // filters
-    for (uint32_t i = c.o_fx + threadIdx.x; i < c.o_cnt + W; i += blockDim.x) g_dsm[i] = 0u;
+    const uint32_t o_end = c.o_cnt + W;
+    for (uint32_t i = c.o_fx + threadIdx.x; i < o_end; i += blockDim.x) g_dsm[i] = 0u;
     __syncthreads();
 
     uint32_t n_in = 0;
@@ -226,7 +227,7 @@ __global__ void __launch_bounds__(GenThreads<A>::value, 1)
 
     // flush the window into the global accumulator (L2 reductions)
     for (uint32_t l = threadIdx.x; l < W; l += blockDim.x) {
-        const unsigned cnt = g_dsm[c.o_cnt + l];
+        const unsigned long long cnt = g_dsm[c.o_cnt + l];
         if (cnt == 0) continue;
         uint32_t rem = l;
         uint64_t b = 0, mul = 1;
@@ -237,7 +238,7 @@ __global__ void __launch_bounds__(GenThreads<A>::value, 1)
             b += (uint64_t)kd * mul;
             mul *= (uint64_t)c.G.res[d];
         }
-        atomicAdd(&c.count[b], (unsigned long long)cnt);
+        atomicAdd(&c.count[b], cnt);
 #pragma unroll
         for (int a = 0; a < A; ++a) {
             if ((c.sum_mask >> a) & 1u) {

@@ -43,19 +43,22 @@ struct DGeom {
 };
 
 // Realised mesh bounds and scales; identical in every CTA of every kernel.
+// ND = compile-time dimensionality (0 = take g.ndim at run time).
+template <int ND = 0>
 __device__ __forceinline__ DGeom load_geom(const Geom &g, const unsigned long long *bounds) {
     DGeom G;
     G.ok = true;
+    const int ndim = ND > 0 ? ND : g.ndim;
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
-        G.res[d] = d < g.ndim ? g.res[d] : 1;
+        G.res[d] = d < ndim ? g.res[d] : 1;
         G.lo[d] = 0.0;
         G.hi[d] = 1.0;
         G.scale[d] = 1.0;
-        if (d >= g.ndim) continue;
+        if (d >= ndim) continue;
         double lo = g.lo[d], hi = g.hi[d];
         if (g.bounds_auto) {
-            unsigned long long elo = bounds[d], nhi = bounds[g.ndim + d];
+            unsigned long long elo = bounds[d], nhi = bounds[ndim + d];
             if (elo == ~0ull || nhi == ~0ull) G.ok = false;  // no non-NaN row anywhere
             lo = dec_total(elo);
             hi = dec_total(~nhi);
@@ -87,7 +90,11 @@ __device__ __forceinline__ bool bin_coords(const DGeom &G, const double (&x)[D],
 }
 
 // ---- fixed-point window sums (see bin_general.cu / bin_fast.cu headers) ----
-constexpr long long FX_OFFSET = 1ll << 54;  // makes every q' positive: q in (-2^54, 2^54)
+// q' = round(v * 2^F) + 2^54 with |round(v * 2^F)| < 2^54, summed exactly in
+// 96 bits; the flush subtracts count * 2^54.  (The count cannot be recovered
+// from the sum alone: sum q / 2^55 is not bounded by 1/2 -- tried and
+// rejected, WE4 catches it -- so windows keep an explicit count.)
+constexpr long long FX_OFFSET = 1ll << 54;
 constexpr unsigned FX_OFFSET_MID = (unsigned)(FX_OFFSET >> 32);
 
 struct FxParam {
@@ -123,9 +130,10 @@ __device__ __forceinline__ unsigned long long fx_quant(const FxParam &P, double 
     return (unsigned long long)(__double2ll_rn(__dmul_rn(v, P.scale)) + FX_OFFSET);
 }
 
-// Exact 96-bit fixed-point window sum of cnt offset values -> f64 (one rounding
-// when |q| < 2^62, else <= 1 ulp).
-__device__ __forceinline__ double fx_to_double(uint32_t lo, uint32_t mid, uint32_t hi, unsigned cnt, double inv_scale) {
+// Exact 96-bit fixed-point sum of cnt offset values -> f64 (one rounding when
+// |q| < 2^62, else <= 1 ulp).
+__device__ __forceinline__ double fx_to_double(uint32_t lo, uint32_t mid, uint32_t hi, unsigned long long cnt,
+                                               double inv_scale) {
     unsigned __int128 qp = ((unsigned __int128)hi << 64) | ((unsigned __int128)mid << 32) | lo;
     __int128 q = (__int128)qp - (__int128)cnt * (__int128)FX_OFFSET;
     double d;
