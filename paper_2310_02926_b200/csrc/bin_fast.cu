@@ -22,7 +22,10 @@ namespace db {
 
 extern __shared__ __align__(16) uint32_t f_dsm[];
 
-constexpr int FAST_THREADS = 1024;
+#ifndef BIN_FAST_THREADS
+#define BIN_FAST_THREADS 1024
+#endif
+constexpr int FAST_THREADS = BIN_FAST_THREADS;
 constexpr int QCAP = 64;            // >= 31 leftover + 32 new items
 constexpr int QWORDS = 3 * QCAP;    // u32 tags[QCAP] + f64 vals[QCAP]
 constexpr uint32_t QBIN = (1u << 29) - 1;
@@ -30,23 +33,28 @@ enum : uint32_t { QK_GLOBAL = 1u, QK_MIN = 2u, QK_MAX = 4u };
 
 int fast_queue_bytes() { return (FAST_THREADS / 32) * QWORDS * 4 + 16; }
 
+// Hot-loop context: only the D used dimensions (so it stays in registers).
+template <int D>
 struct FastCtx {
-    DGeom G;
-    WinGeom w;
+    double lo[D], hi[D], scale[D];
+    int resm1[D];
+    int wo[D];
+    unsigned we[D];
+    uint32_t W;
     FxParam fx;
     uint32_t o_fx, o_cnt;  // word offsets (filters at 0)
 };
 
 template <int D, int A, int SM, int MM>
-__device__ __forceinline__ uint32_t fast_row(const FastCtx &c, const double (&x)[D], double v, bool valid,
+__device__ __forceinline__ uint32_t fast_row(const FastCtx<D> &c, const double (&x)[D], double v, bool valid,
                                              uint32_t &n_in) {
     constexpr bool HS = A == 1 && SM == 1, HM = A == 1 && MM == 1;
     bool ok = valid;
     int k[D];
 #pragma unroll
     for (int d = 0; d < D; ++d) {
-        ok = ok && (c.G.lo[d] <= x[d]) && (x[d] <= c.G.hi[d]);
-        k[d] = min(floor_nonneg(__dmul_rn(__dsub_rn(x[d], c.G.lo[d]), c.G.scale[d])), c.w.resm1[d]);
+        ok = ok && (c.lo[d] <= x[d]) && (x[d] <= c.hi[d]);
+        k[d] = min(floor_nonneg(__dmul_rn(__dsub_rn(x[d], c.lo[d]), c.scale[d])), c.resm1[d]);
     }
     if (!ok) return 0u;
     ++n_in;
@@ -54,16 +62,16 @@ __device__ __forceinline__ uint32_t fast_row(const FastCtx &c, const double (&x)
     uint32_t l = 0;
 #pragma unroll
     for (int d = D - 1; d >= 0; --d) {
-        const unsigned r = (unsigned)(k[d] - c.w.wo[d]);
-        inw = inw && (r < c.w.we[d]);
-        l = l * c.w.we[d] + r;
+        const unsigned r = (unsigned)(k[d] - c.wo[d]);
+        inw = inw && (r < c.we[d]);
+        l = l * c.we[d] + r;
     }
     uint32_t b = (uint32_t)k[0];
-    if (D >= 2) b += (uint32_t)(c.w.resm1[0] + 1) * (uint32_t)k[1];
-    if (D >= 3) b += (uint32_t)(c.w.resm1[0] + 1) * (uint32_t)(c.w.resm1[1] + 1) * (uint32_t)k[2];
+    if (D >= 2) b += (uint32_t)(c.resm1[0] + 1) * (uint32_t)k[1];
+    if (D >= 3) b += (uint32_t)(c.resm1[0] + 1) * (uint32_t)(c.resm1[D > 2 ? 1 : 0] + 1) * (uint32_t)k[D > 2 ? 2 : 0];
     if (!inw) return (QK_GLOBAL << 29) | b;
     atomicAdd(&f_dsm[c.o_cnt + l], 1u);
-    const uint32_t W = c.w.W;
+    const uint32_t W = c.W;
     uint32_t tag = 0;
     if (HS) {
         const uint32_t w0 = c.o_fx + l;
@@ -157,21 +165,130 @@ __device__ __forceinline__ void fast_push(uint32_t qb, uint32_t &qn, uint32_t ta
     }
 }
 
+constexpr int SAMPLE_PAIRS = 2;  // per thread, spread over the thread's range (the first is reused)
+
+// The CTA's window: coarse histogram of 4 sample pairs per thread (spread over
+// the thread's range) in the still-unused dynamic shared memory, then the best
+// box (dev_common.cuh pick_box); also the largest exponent of the attribute.
+// Everything indexed statically (D is a template parameter) so no scratch goes
+// to local memory and the hot loop keeps the geometry in registers.
+template <int D, int A>
+__device__ __forceinline__ void fast_choose_window(const DGeom G, const WinPlan P, const double2 *cx0,
+                                                   const double2 *cx1, const double2 *cx2,
+                                                   const double2 *cv, uint32_t p0, uint32_t nthr, uint32_t npairs,
+                                                bool want_exp, unsigned long long *s_best, int *s_origin,
+                                                unsigned *s_exp) {
+    if (threadIdx.x == 0) *s_exp = 0u;
+    const bool hist = !P.full && !P.skip;
+    if (hist)
+        for (int i = threadIdx.x; i < WIN_CELLS; i += FAST_THREADS) f_dsm[i] = 0u;
+    const uint32_t iters = p0 < npairs ? (npairs - 1 - p0) / nthr + 1 : 0u;
+    const double2 *const cx[3] = {cx0, cx1, cx2};
+    double2 sx[SAMPLE_PAIRS][D], sv[SAMPLE_PAIRS];
+#pragma unroll
+    for (int k = 0; k < SAMPLE_PAIRS; ++k) {
+        const uint32_t it = (uint32_t)(((uint64_t)iters * k) / SAMPLE_PAIRS);
+        const bool ok = it < iters;
+        const uint32_t q = p0 + it * nthr;
+#pragma unroll
+        for (int d = 0; d < D; ++d) sx[k][d] = ok ? __ldcs(cx[d] + q) : make_double2(0.0, 0.0);
+        sv[k] = (ok && A == 1) ? __ldcs(cv + q) : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+    unsigned emax = 0u;
+#pragma unroll
+    for (int k = 0; k < SAMPLE_PAIRS; ++k) {
+        const uint32_t it = (uint32_t)(((uint64_t)iters * k) / SAMPLE_PAIRS);
+        if (it >= iters) continue;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const double v = h ? sv[k].y : sv[k].x;
+            const unsigned eb = ((unsigned)__double2hiint(v) >> 20) & 0x7ffu;
+            if (A == 1 && eb != 0x7ffu && eb > emax) emax = eb;
+            if (!hist) continue;
+            bool inside = true;
+            int cell = 0, mul = 1;
+#pragma unroll
+            for (int d = 0; d < D; ++d) {
+                const double x = h ? sx[k][d].y : sx[k][d].x;
+                inside = inside && (G.lo[d] <= x) && (x <= G.hi[d]);
+                const int kd = min(floor_nonneg(__dmul_rn(__dsub_rn(x, G.lo[d]), G.scale[d])), G.res[d] - 1);
+                cell += (kd / P.cs[d]) * mul;
+                mul *= P.nc[d];
+            }
+            if (inside) atomicAdd(&f_dsm[cell], 1u);
+        }
+    }
+    if (want_exp) {
+        const unsigned m = __reduce_max_sync(0xffffffffu, emax);
+        if ((threadIdx.x & 31) == 0 && m) atomicMax(s_exp, m);
+    }
+    __syncthreads();
+    if (hist) {
+        pick_box<D>(P, G.res[0], G.res[1], G.res[2], f_dsm, s_best, s_origin);
+    } else if (threadIdx.x < 3) {
+        s_origin[threadIdx.x] = 0;
+    }
+    __syncthreads();  // the histogram scratch becomes the window after this
+}
+
 template <int D, int A, int SM, int MM>
 __global__ void __launch_bounds__(FAST_THREADS, 1)
-    k_bin_fast(Geom g, Inputs in, Accum acc, uint32_t npairs, int head) {
+    k_bin_fast(Geom g, Inputs in, Accum acc, uint32_t npairs, int head, int wcap) {
     constexpr bool HS = A == 1 && SM == 1, HM = A == 1 && MM == 1;
-    FastCtx c;
-    c.G = load_geom<D>(g, acc.bounds);
-    if (!c.G.ok) return;  // degenerate auto bounds: finalize reports it
-    c.w = load_window(c.G, acc.window, D);
-    const uint32_t W = c.w.W;
-    c.o_fx = HM ? 2u * W : 0u;
-    c.o_cnt = c.o_fx + (HS ? 3u * W : 0u);
-    c.fx = fx_param(A == 1 ? acc.fxexp[0] : 0u);
+    __shared__ unsigned long long s_best[FAST_THREADS / 32];
+    __shared__ int s_origin[3];
+    __shared__ unsigned s_exp;
+    FastCtx<D> c;
     unsigned long long *const count = acc.count;
     double *const sum = acc.sum;
     ulonglong2 *const mm = (ulonglong2 *)acc.mm;
+
+    const double2 *cx[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) cx[d] = (const double2 *)(in.ax[d] + head);
+    const double2 *cv = (const double2 *)((A == 1 ? in.at[0] : in.ax[0]) + head);
+    const uint32_t nthr = gridDim.x * FAST_THREADS;
+    const uint32_t p0 = blockIdx.x * FAST_THREADS + threadIdx.x;
+    int res[3];
+    {
+        const DGeom G = load_geom<D>(g, acc.bounds);
+        if (!G.ok) return;  // degenerate auto bounds: finalize reports it (uniform: every thread returns)
+        // ---- this CTA's window, from a sample of its own rows
+        const WinPlan P = window_plan(G, D, wcap);
+        fast_choose_window<D, A>(G, P, cx[0], cx[D > 1 ? 1 : 0], cx[D > 2 ? 2 : 0], cv, p0, nthr, npairs, HS, s_best,
+                                 s_origin, &s_exp);
+        c.W = 1;
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+            c.lo[d] = G.lo[d];
+            c.hi[d] = G.hi[d];
+            c.scale[d] = G.scale[d];
+            c.resm1[d] = G.res[d] - 1;
+            c.wo[d] = s_origin[d];
+            c.we[d] = P.skip ? 0u : (unsigned)P.e[d];
+            c.W *= c.we[d];
+        }
+#pragma unroll
+        for (int d = 0; d < 3; ++d) res[d] = G.res[d];
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {  // reported window (CTA 0's); static indices only
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            acc.window[d] = d < D ? c.wo[d < D ? d : 0] : 0;
+            acc.window[3 + d] = d < D ? (int)c.we[d < D ? d : 0] : 1;
+        }
+    }
+    c.fx = fx_param(HS ? s_exp : 0u);
+    double2 bx[D], bv = make_double2(0.0, 0.0);
+    if (p0 < npairs) {
+#pragma unroll
+        for (int d = 0; d < D; ++d) bx[d] = __ldcs(cx[d] + p0);
+        if (A == 1) bv = __ldcs(cv + p0);
+    }
+    const uint32_t W = c.W;
+    c.o_fx = HM ? 2u * W : 0u;
+    c.o_cnt = c.o_fx + (HS ? 3u * W : 0u);
 
     for (uint32_t i = threadIdx.x; i < c.o_fx; i += FAST_THREADS) f_dsm[i] = ~0u;  // min/max filters
     const uint32_t o_end = c.o_cnt + W;
@@ -181,20 +298,7 @@ __global__ void __launch_bounds__(FAST_THREADS, 1)
     uint32_t qn = 0;
     __syncthreads();
 
-    const double2 *cx[D];
-#pragma unroll
-    for (int d = 0; d < D; ++d) cx[d] = (const double2 *)(in.ax[d] + head);
-    const double2 *cv = (const double2 *)((A == 1 ? in.at[0] : in.ax[0]) + head);
-
     uint32_t n_in = 0, rows = 0;
-    const uint32_t nthr = gridDim.x * FAST_THREADS;
-    const uint32_t p0 = blockIdx.x * FAST_THREADS + threadIdx.x;
-    double2 bx[D], bv = make_double2(0.0, 0.0);
-    if (p0 < npairs) {
-#pragma unroll
-        for (int d = 0; d < D; ++d) bx[d] = __ldcs(cx[d] + p0);
-        if (A == 1) bv = __ldcs(cv + p0);
-    }
     for (uint32_t pb = p0 - lane; pb < npairs; pb += nthr) {  // warp-uniform trip count
         const uint32_t pc = pb + lane;
         const bool valid = pc < npairs;
@@ -253,10 +357,10 @@ __global__ void __launch_bounds__(FAST_THREADS, 1)
         uint32_t rem = l, b = 0, mul = 1;
 #pragma unroll
         for (int d = 0; d < D; ++d) {
-            const uint32_t kd = rem % c.w.we[d] + (uint32_t)c.w.wo[d];
-            rem /= c.w.we[d];
+            const uint32_t kd = rem % c.we[d] + (uint32_t)c.wo[d];
+            rem /= c.we[d];
             b += kd * mul;
-            mul *= (uint32_t)c.G.res[d];
+            mul *= (uint32_t)res[d];
         }
         atomicAdd(&count[b], cnt);
         if (HS) {
@@ -282,7 +386,7 @@ bool fast_eligible(const Inputs &in, const Accum &acc, int ndim) {
 
 template <int D, int A, int SM, int MM>
 static cudaError_t launch_fast_t(const Geom &g, const Inputs &in, const Accum &acc, const LaunchCfg &lc, int smem,
-                                 cudaStream_t s) {
+                                 int wcap, cudaStream_t s) {
     const int head = ((uintptr_t)in.ax[0] & 15u) ? 1 : 0;
     const uint32_t npairs = (uint32_t)((in.n - head) / 2);
     int blocks = lc.sms;  // one persistent CTA per SM: the whole shared memory holds the window
@@ -291,26 +395,26 @@ static cudaError_t launch_fast_t(const Geom &g, const Inputs &in, const Accum &a
     auto kern = k_bin_fast<D, A, SM, MM>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    kern<<<blocks, FAST_THREADS, smem, s>>>(g, in, acc, npairs, head);
+    kern<<<blocks, FAST_THREADS, smem, s>>>(g, in, acc, npairs, head, wcap);
     return cudaGetLastError();
 }
 
 template <int D>
 static cudaError_t launch_fast_d(const Geom &g, const Inputs &in, const Accum &acc, const LaunchCfg &lc, int smem,
-                                 cudaStream_t s) {
-    if (in.nattr == 0 || !(acc.load_mask & 1u)) return launch_fast_t<D, 0, 0, 0>(g, in, acc, lc, smem, s);
+                                 int wcap, cudaStream_t s) {
+    if (in.nattr == 0 || !(acc.load_mask & 1u)) return launch_fast_t<D, 0, 0, 0>(g, in, acc, lc, smem, wcap, s);
     const bool sm = acc.sum_mask & 1u, mm = acc.mm_mask & 1u;
-    if (sm && mm) return launch_fast_t<D, 1, 1, 1>(g, in, acc, lc, smem, s);
-    if (sm) return launch_fast_t<D, 1, 1, 0>(g, in, acc, lc, smem, s);
-    return launch_fast_t<D, 1, 0, 1>(g, in, acc, lc, smem, s);
+    if (sm && mm) return launch_fast_t<D, 1, 1, 1>(g, in, acc, lc, smem, wcap, s);
+    if (sm) return launch_fast_t<D, 1, 1, 0>(g, in, acc, lc, smem, wcap, s);
+    return launch_fast_t<D, 1, 0, 1>(g, in, acc, lc, smem, wcap, s);
 }
 
 cudaError_t launch_bin_fast(const Geom &g, const Inputs &in, const Accum &acc, const LaunchCfg &lc, int smem,
-                            cudaStream_t s) {
+                            int wcap, cudaStream_t s) {
     switch (g.ndim) {
-    case 1: return launch_fast_d<1>(g, in, acc, lc, smem, s);
-    case 2: return launch_fast_d<2>(g, in, acc, lc, smem, s);
-    default: return launch_fast_d<3>(g, in, acc, lc, smem, s);
+    case 1: return launch_fast_d<1>(g, in, acc, lc, smem, wcap, s);
+    case 2: return launch_fast_d<2>(g, in, acc, lc, smem, wcap, s);
+    default: return launch_fast_d<3>(g, in, acc, lc, smem, wcap, s);
     }
 }
 

@@ -96,7 +96,7 @@ struct Accum {
     unsigned long long *mm;     // nmm * nbins * 2: {enc(min), ~enc(max)}
     unsigned long long *bounds; // 2*ndim: {enc(lo_d)..., ~enc(hi_d)...}
     int32_t *window;            // 6 ints: origin[3], extent[3]
-    uint32_t *whist;            // 4096 coarse-cell sample counts (window choice)
+    uint32_t *whist;            // 4096 coarse-cell sample counts + [4096] last-CTA ticket (window choice)
     uint32_t *fxexp;            // 16: max biased exponent of each summed attribute over the sample
     double *omin, *omax, *oavg; // outputs
     uint64_t nbins;
@@ -117,14 +117,15 @@ struct LaunchCfg {
 };
 
 // Each returns cudaError_t of the launch.
-cudaError_t launch_init(const Accum &acc, int ndim, cudaStream_t s);
+cudaError_t launch_init(const Geom &g, const Inputs &in, const Accum &acc, int wcap, bool choose_window,
+                        cudaStream_t s);
 cudaError_t launch_bounds(const Geom &g, const Inputs &in, const Accum &acc, const LaunchCfg &lc,
                           cudaStream_t s);
 cudaError_t launch_window(const Geom &g, const Inputs &in, const Accum &acc, int wcap, cudaStream_t s);
 cudaError_t launch_bin_general(const Geom &g, const Inputs &in, const Accum &acc, const LaunchCfg &lc, int smem,
                                cudaStream_t s);
 cudaError_t launch_bin_fast(const Geom &g, const Inputs &in, const Accum &acc, const LaunchCfg &lc, int smem,
-                            cudaStream_t s);
+                            int wcap, cudaStream_t s);
 bool fast_eligible(const Inputs &in, const Accum &acc, int ndim);
 int fast_queue_bytes();
 cudaError_t launch_finalize(const Geom &g, const Accum &acc, Meta *meta_dev, int64_t n_rows_local,

@@ -178,4 +178,149 @@ __device__ __forceinline__ WinGeom load_window(const DGeom &G, const int32_t *wi
     return w;
 }
 
+// ---- window planning (shared by the window kernels and k_bin_fast) ----
+constexpr int WIN_CELLS = 4096;
+
+struct WinPlan {
+    int e[3], cs[3], nc[3];
+    bool full, skip;
+};
+
+__device__ __forceinline__ WinPlan window_plan(const DGeom &G, int D, int wcap) {
+    WinPlan P;
+    long long total = (long long)G.res[0] * G.res[1] * G.res[2];
+    P.skip = !G.ok || wcap <= 0;
+    P.full = !P.skip && total <= wcap;
+    for (int d = 0; d < 3; ++d) P.e[d] = P.full ? G.res[d] : 1;
+    if (!P.full && !P.skip) {
+        const int *res = G.res;
+        if (D == 1) {
+            P.e[0] = min(res[0], wcap);
+        } else if (D == 2) {
+            int s = (int)floor(sqrt((double)wcap));
+            P.e[0] = min(res[0], max(1, s));
+            P.e[1] = min(res[1], wcap / P.e[0]);
+            if (P.e[1] == res[1]) P.e[0] = min(res[0], wcap / res[1]);
+        } else {
+            int c = (int)floor(cbrt((double)wcap));
+            P.e[0] = min(res[0], max(1, c));
+            P.e[1] = min(res[1], max(1, c));
+            P.e[2] = min(res[2], wcap / (P.e[0] * P.e[1]));
+            if (P.e[2] == res[2]) {
+                int s = (int)floor(sqrt((double)(wcap / res[2])));
+                P.e[0] = min(res[0], max(1, s));
+                P.e[1] = min(res[1], wcap / (res[2] * P.e[0]));
+            }
+        }
+    }
+    int ncmax = D == 1 ? WIN_CELLS : (D == 2 ? 64 : 16);
+    for (int d = 0; d < 3; ++d) {
+        P.cs[d] = (G.res[d] + ncmax - 1) / ncmax;
+        P.nc[d] = (G.res[d] + P.cs[d] - 1) / P.cs[d];
+    }
+    return P;
+}
+
+// Inclusive scan of one line of <= 64 cells (stride `step`) by one warp.
+__device__ __forceinline__ void warp_line_scan(unsigned *h, int base, int step, int len) {
+    const int lane = threadIdx.x & 31;
+    const int i0 = 2 * lane, i1 = 2 * lane + 1;
+    unsigned a = i0 < len ? h[base + i0 * step] : 0u, b = i1 < len ? h[base + i1 * step] : 0u;
+    unsigned s = a + b;
+    for (int o = 1; o < 32; o <<= 1) {
+        unsigned y = __shfl_up_sync(0xffffffffu, s, o);
+        if (lane >= o) s += y;
+    }
+    const unsigned pre = s - a - b;
+    if (i0 < len) h[base + i0 * step] = pre + a;
+    if (i1 < len) h[base + i1 * step] = pre + a + b;
+}
+
+
+// Summed-area table of the coarse histogram `hist` (shared memory, nc cells),
+// then the box of wc = e/cs coarse cells with the most samples (ties -> lowest
+// index).  All threads of the CTA take part (blockDim >= 256); the box origin
+// in bins is written to origin[0..2] (shared) and is valid after the return.
+template <int D>
+__device__ __forceinline__ void pick_box(const WinPlan P, const int res0, const int res1, const int res2,
+                                         unsigned *hist, unsigned long long *best, int *origin) {
+    const int res[3] = {res0, res1, res2};  // by value: no pointer into the caller's geometry
+    const int *nc = P.nc;
+    const int ncell = nc[0] * nc[1] * nc[2];
+    const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+        const int len = nc[d];
+        const int lines = ncell / len;
+        const int step = d == 0 ? 1 : (d == 1 ? nc[0] : nc[0] * nc[1]);
+        if (len <= 64) {
+            for (int ln = warp; ln < lines; ln += nwarps) {
+                int base;
+                if (d == 0) base = ln * nc[0];
+                else if (d == 1) base = (ln % nc[0]) + (ln / nc[0]) * nc[0] * nc[1];
+                else base = ln;
+                warp_line_scan(hist, base, step, len);
+            }
+            __syncthreads();
+        } else {  // 1D: Hillis-Steele over up to WIN_CELLS cells
+            for (int off = 1; off < len; off <<= 1) {
+                unsigned vv[16];
+#pragma unroll
+                for (int r = 0; r < 16; ++r) {
+                    const int i = threadIdx.x + r * blockDim.x;
+                    vv[r] = (i < len && i >= off) ? hist[i - off] : 0u;
+                }
+                __syncthreads();
+#pragma unroll
+                for (int r = 0; r < 16; ++r) {
+                    const int i = threadIdx.x + r * blockDim.x;
+                    if (i < len) hist[i] += vv[r];
+                }
+                __syncthreads();
+            }
+        }
+    }
+    int wc[3], np[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        wc[d] = d < D ? max(1, P.e[d] / P.cs[d]) : 1;
+        np[d] = nc[d] - wc[d] + 1;
+    }
+    auto sat = [&](int i0, int i1, int i2) -> long long {
+        if (i0 < 0 || i1 < 0 || i2 < 0) return 0;
+        return hist[i0 + nc[0] * (i1 + nc[1] * i2)];
+    };
+    unsigned long long mybest = 0;  // (count << 32) | (0xffffffff - candidate)
+    const int ncand = np[0] * np[1] * np[2];
+    for (int c = threadIdx.x; c < ncand; c += blockDim.x) {
+        const int o0 = c % np[0], o1 = (c / np[0]) % np[1], o2 = c / (np[0] * np[1]);
+        const int a0 = o0 - 1, a1 = o1 - 1, a2 = o2 - 1;
+        const int b0 = o0 + wc[0] - 1, b1 = o1 + wc[1] - 1, b2 = o2 + wc[2] - 1;
+        const long long v = sat(b0, b1, b2) - sat(a0, b1, b2) - sat(b0, a1, b2) - sat(b0, b1, a2) + sat(a0, a1, b2) +
+                            sat(a0, b1, a2) + sat(b0, a1, a2) - sat(a0, a1, a2);
+        const unsigned long long key = ((unsigned long long)v << 32) | (0xffffffffull - (unsigned)c);
+        mybest = key > mybest ? key : mybest;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long w = __shfl_xor_sync(0xffffffffu, mybest, o);
+        mybest = w > mybest ? w : mybest;
+    }
+    if ((threadIdx.x & 31) == 0) best[warp] = mybest;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long bb = 0;
+        for (int i = 0; i < nwarps; ++i) bb = best[i] > bb ? best[i] : bb;
+        const int c = (int)(0xffffffffull - (bb & 0xffffffffull));
+        const int o[3] = {c % np[0], (c / np[0]) % np[1], c / (np[0] * np[1])};
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            int org = o[d] * P.cs[d];
+            if (org + P.e[d] > res[d]) org = res[d] - P.e[d];
+            origin[d] = org;
+        }
+    }
+    __syncthreads();
+}
+
 }  // namespace db

@@ -24,6 +24,7 @@ struct Slot {
     cudaEvent_t done = nullptr, released = nullptr;
     cudaEvent_t ev[EV_N] = {};
     bool prof_pending = false;
+    bool meta_valid = false;
     uint64_t ticket = 0;
     bool used = false;
     cudaStream_t stream = nullptr;
@@ -47,6 +48,7 @@ struct bin_handle {
     int device = 0;
     ncclComm_t comm = nullptr;
     cudaStream_t side = nullptr;
+    cudaStream_t meta_stream = nullptr;
     Slot slot[2];
     uint64_t next_ticket = 1;
     Stage stage[2][BIN_MAX_DIM + BIN_MAX_ATTR];
@@ -92,11 +94,12 @@ static int alloc_slot(bin_handle *h, Slot &s) {
     size_t o_bounds = o_mm + al(B * 16 * h->nmm);
     size_t o_window = o_bounds + al(6 * 8);
     size_t o_whist = o_window + al(8 * 4);
-    size_t o_fxexp = o_whist + al(4096 * 4);
+    size_t o_fxexp = o_whist + al(4097 * 4);
     size_t o_omin = o_fxexp + al(16 * 4);
     size_t o_omax = o_omin + al(B * 8 * h->nmm);
     size_t o_oavg = o_omax + al(B * 8 * h->nmm);
-    size_t total = o_oavg + al(B * 8 * h->nsum);
+    size_t o_meta = o_oavg + al(B * 8 * h->nsum);
+    size_t total = o_meta + al(sizeof(Meta));
     unsigned char *base = nullptr;
     cudaError_t e = cudaMalloc(&base, total);
     if (e != cudaSuccess) {
@@ -105,6 +108,7 @@ static int alloc_slot(bin_handle *h, Slot &s) {
     }
     count_alloc((int64_t)total);
     s.dev_bytes = total;
+    if ((e = cudaMemset(base, 0, total)) != cudaSuccess) return cuda_error(e, "bin_init memset");
     s.acc.count = (unsigned long long *)(base + o_count);
     s.acc.sum = (double *)(base + o_sum);
     s.acc.mm = (unsigned long long *)(base + o_mm);
@@ -121,10 +125,12 @@ static int alloc_slot(bin_handle *h, Slot &s) {
     s.acc.sum_mask = h->sum_mask;
     s.acc.mm_mask = h->mm_mask;
     s.acc.load_mask = h->load_mask;
-    DB_CUDA(cudaHostAlloc((void **)&s.meta_h, sizeof(Meta), cudaHostAllocMapped | cudaHostAllocPortable));
+    // result meta: written by the finalize kernel in device memory, copied to this
+    // pinned mirror only when the host asks (bin_wait) -- no PCIe writes in the step
+    DB_CUDA(cudaHostAlloc((void **)&s.meta_h, sizeof(Meta), cudaHostAllocPortable));
     count_alloc((int64_t)sizeof(Meta));
     memset(s.meta_h, 0, sizeof(Meta));
-    DB_CUDA(cudaHostGetDevicePointer((void **)&s.meta_d, s.meta_h, 0));
+    s.meta_d = (Meta *)(base + o_meta);
     DB_CUDA(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
     DB_CUDA(cudaEventCreateWithFlags(&s.released, cudaEventDisableTiming));
     for (auto &ev : s.ev) DB_CUDA(cudaEventCreate(&ev));
@@ -243,6 +249,8 @@ int bin_init(const bin_spec_t *spec, const bin_placement_t *place, const bin_com
     };
     if ((ce = cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking)) != cudaSuccess)
         return fail(cuda_error(ce, "cudaStreamCreate"));
+    if ((ce = cudaStreamCreateWithFlags(&h->meta_stream, cudaStreamNonBlocking)) != cudaSuccess)
+        return fail(cuda_error(ce, "cudaStreamCreate"));
     cudaDeviceGetAttribute(&h->lc.sms, cudaDevAttrMultiProcessorCount, dev);
     cudaDeviceGetAttribute(&h->lc.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     Accum probe{};
@@ -251,7 +259,8 @@ int bin_init(const bin_spec_t *spec, const bin_placement_t *place, const bin_com
     probe.nbins = B;
     const int bpb = window_bytes_per_bin(probe);
     const int qbytes = (spec->nattr <= 1 && B < (1ull << 29)) ? fast_queue_bytes() : 0;  // k_bin_fast queues
-    h->wcap = (h->lc.smem_optin - qbytes) / bpb;
+    const int static_smem = 1024;  // kernels' static __shared__ (k_bin_fast: window-pick scratch)
+    h->wcap = (h->lc.smem_optin - static_smem - qbytes) / bpb;
     h->smem_bytes = (int)((uint64_t)h->wcap >= B ? B * bpb : (uint64_t)h->wcap * bpb);
     h->smem_bytes = ((h->smem_bytes + 15) & ~15) + qbytes;
     for (auto &s : h->slot)
@@ -328,6 +337,7 @@ int bin_execute(bin_handle_t *h, bin_array_t *const *axes, int32_t naxes, bin_ar
     if (S.used && S.stream != s) DB_CUDA(cudaStreamWaitEvent(s, S.done, 0));
     S.ticket = t;
     S.used = true;
+    S.meta_valid = false;
     S.stream = s;
     S.launches = 0;
     S.bin_launches = 0;
@@ -398,8 +408,12 @@ int bin_execute(bin_handle_t *h, bin_array_t *const *axes, int32_t naxes, bin_ar
     };
     int rc;
     if ((rc = rec(EV_INIT0))) return rc;
-    // ---- a3: accumulator identities
-    if ((e = launch_init(S.acc, geom.ndim, s)) != cudaSuccess) return cuda_error(e, "init kernel");
+    // ---- a3: accumulator identities (+ the window choice when the bounds are manual
+    // and the general kernel will run; k_bin_fast chooses its windows per CTA)
+    const bool fast = n > 0 && !h->spec.deterministic && fast_eligible(in, S.acc, geom.ndim);
+    const bool window_in_prep = !geom.bounds_auto && !h->spec.deterministic && !fast;
+    if ((e = launch_init(geom, in, S.acc, h->wcap, window_in_prep, s)) != cudaSuccess)
+        return cuda_error(e, "init kernel");
     S.launches++;
     if ((rc = rec(EV_INIT1))) return rc;
     // ---- a2: automatic bounds (+ cross-rank Min, reading R3)
@@ -424,14 +438,15 @@ int bin_execute(bin_handle_t *h, bin_array_t *const *axes, int32_t naxes, bin_ar
         variant = 3;
     } else {
         // ---- hot-window choice, then a4 + a5
-        if ((e = launch_window(geom, in, S.acc, h->wcap, s)) != cudaSuccess) return cuda_error(e, "window kernel");
-        S.launches += 2;
+        if (!window_in_prep && !fast) {
+            if ((e = launch_window(geom, in, S.acc, h->wcap, s)) != cudaSuccess) return cuda_error(e, "window kernel");
+            S.launches += 1;
+        }
         if ((rc = rec(EV_WINDOW1))) return rc;
         if (n / h->lc.sms >= (int64_t)0xffffffffLL)
             return set_error(BIN_EINVAL, "%lld rows per call exceed the per-CTA u32 window counters", (long long)n);
-        const bool fast = n > 0 && fast_eligible(in, S.acc, geom.ndim);
         if (n > 0) {
-            e = fast ? launch_bin_fast(geom, in, S.acc, h->lc, h->smem_bytes, s)
+            e = fast ? launch_bin_fast(geom, in, S.acc, h->lc, h->smem_bytes, h->wcap, s)
                      : launch_bin_general(geom, in, S.acc, h->lc, h->smem_bytes, s);
             if (e != cudaSuccess) return cuda_error(e, "bin kernel");
             S.launches++, S.bin_launches++;
@@ -461,7 +476,6 @@ int bin_execute(bin_handle_t *h, bin_array_t *const *axes, int32_t naxes, bin_ar
     }
     if ((rc = rec(EV_COMBINE1))) return rc;
     // ---- a7: finalize
-    S.meta_h->done = 0;
     if ((e = launch_finalize(geom, S.acc, S.meta_d, n, variant, s)) != cudaSuccess) return cuda_error(e, "finalize kernel");
     S.launches++;
     S.variant = variant;
@@ -492,9 +506,20 @@ int bin_inputs_released(bin_handle_t *h, uint64_t ticket, bin_event_t *ev) {
     return BIN_OK;
 }
 
+// Copies a completed slot's result meta (device) to its pinned mirror on the
+// handle's meta stream (non-blocking: it does not serialise with the work).
+static int fetch_meta(bin_handle *h, Slot &S) {
+    if (S.meta_valid) return BIN_OK;
+    DB_CUDA(cudaMemcpyAsync(S.meta_h, S.meta_d, sizeof(Meta), cudaMemcpyDeviceToHost, h->meta_stream));
+    DB_CUDA(cudaStreamSynchronize(h->meta_stream));
+    S.meta_valid = true;
+    return BIN_OK;
+}
+
 static void accumulate_profile(bin_handle *h, Slot &S) {
     if (!S.prof_pending) return;
     S.prof_pending = false;
+    fetch_meta(h, S);
     float ms[EV_N] = {};
     for (int k = 1; k < EV_N; ++k) cudaEventElapsedTime(&ms[k], S.ev[k - 1], S.ev[k]);
     cudaGetLastError();
@@ -520,6 +545,8 @@ int bin_wait(bin_handle_t *h, uint64_t ticket) {
     DeviceGuard g(h->device);
     cudaError_t e = cudaEventSynchronize(S->done);
     if (e != cudaSuccess) return cuda_error(e, "bin_wait");
+    int rc = fetch_meta(h, *S);
+    if (rc) return rc;
     accumulate_profile(h, *S);
     if (S->meta_h->status == BIN_EDEGENERATE)
         return set_error(BIN_EDEGENERATE, "auto bounds: no finite rows in total, or an infinite/unrecoverable axis");
@@ -612,7 +639,9 @@ int bin_finalize(bin_handle_t *h) {
             h->gather = nullptr;
         }
         if (h->side) cudaStreamDestroy(h->side);
+        if (h->meta_stream) cudaStreamDestroy(h->meta_stream);
         h->side = nullptr;
+        h->meta_stream = nullptr;
     }
     h->finalized = true;
     delete h;

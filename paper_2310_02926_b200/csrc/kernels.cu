@@ -24,27 +24,136 @@
 #include "dev_common.cuh"
 
 namespace db {
-// ---------------------------------------------------------------- init [a3]
-constexpr int WIN_CELLS_INIT = 4096;
-__global__ void k_init(Accum acc, int ndim) {
-    const uint64_t nb = acc.nbins;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    for (int64_t i = t0; i < (int64_t)nb + 2; i += stride) acc.count[i] = 0ull;
-    for (int64_t i = t0; i < (int64_t)(nb * acc.nsum); i += stride) acc.sum[i] = 0.0;
-    ulonglong2 ident = make_ulonglong2(~0ull, ~0ull);
-    for (int64_t i = t0; i < (int64_t)(nb * acc.nmm); i += stride) ((ulonglong2 *)acc.mm)[i] = ident;
-    if (t0 < 2 * ndim) acc.bounds[t0] = ~0ull;
-    for (int64_t i = t0; i < WIN_CELLS_INIT; i += stride) acc.whist[i] = 0u;
-    if (t0 < BIN_MAX_ATTR) acc.fxexp[t0] = 0u;
+// ---------------------------------------------------------------- init [a3] + window
+// k_prep: accumulator identities (reading R5) in CTAs 1..; with manual bounds
+// CTA 0 meanwhile chooses the window.  k_window does the window choice after
+// the automatic bounds are known.  The window -- the box of bins each binning
+// CTA privatises in shared memory; only speed depends on it -- is the box
+// position holding the most of 16,384 strided sample rows (coarse histogram +
+// summed-area table).  The sample also records the largest exponent of each
+// summed attribute (fixed-point scale, dev_common.cuh fx_param); fxexp is
+// cleared by the finalize kernel for the next execute on the slot.
+constexpr int WIN_SAMPLES = 16384;
+constexpr int PREP_THREADS = 512;
+constexpr int WIN_BATCH = 8;  // sample rows per thread in flight
+
+// Best box from the coarse histogram in shared memory -> acc.window.
+__device__ void window_pick(const Geom &g, const DGeom &G, const WinPlan &P, const Accum &acc, unsigned *hist,
+                            unsigned long long *best) {
+    __shared__ int origin[3];
+    if (P.skip || P.full) {
+        if (threadIdx.x < 3) {
+            acc.window[threadIdx.x] = 0;
+            acc.window[3 + threadIdx.x] = P.skip ? 0 : G.res[threadIdx.x];
+        }
+        return;
+    }
+    switch (g.ndim) {
+    case 1: pick_box<1>(P, G.res[0], G.res[1], G.res[2], hist, best, origin); break;
+    case 2: pick_box<2>(P, G.res[0], G.res[1], G.res[2], hist, best, origin); break;
+    default: pick_box<3>(P, G.res[0], G.res[1], G.res[2], hist, best, origin); break;
+    }
+    if (threadIdx.x < 3) {
+        acc.window[threadIdx.x] = origin[threadIdx.x];
+        acc.window[3 + threadIdx.x] = P.e[threadIdx.x];
+    }
 }
 
-cudaError_t launch_init(const Accum &acc, int ndim, cudaStream_t s) {
-    int64_t work = (int64_t)acc.nbins * (1 + acc.nsum + acc.nmm);
-    int64_t blocks = (work / 4 + 255) / 256;
-    if (blocks < 1) blocks = 1;
-    if (blocks > 148 * 8) blocks = 148 * 8;
-    k_init<<<(unsigned)blocks, 256, 0, s>>>(acc, ndim);
+// One CTA: sample, coarse histogram in shared memory, pick.
+__device__ __forceinline__ void window_choose(const Geom &g, const Inputs &in, const Accum &acc, int wcap) {
+    __shared__ unsigned hist[WIN_CELLS];
+    __shared__ unsigned long long best[PREP_THREADS / 32];
+    const DGeom G = load_geom(g, acc.bounds);
+    const WinPlan P = window_plan(G, g.ndim, wcap);
+    const int D = g.ndim;
+    for (int i = threadIdx.x; i < WIN_CELLS; i += blockDim.x) hist[i] = 0u;
+    __syncthreads();
+    const bool work = !P.skip && in.n > 0;
+    const int64_t S = in.n < WIN_SAMPLES ? in.n : WIN_SAMPLES;
+    const int64_t stride = work ? in.n / S : 1;
+    // largest exponent of each summed attribute over the sample
+    for (int a = 0; work && a < in.nattr; ++a) {
+        if (!((acc.sum_mask >> a) & 1u)) continue;
+        unsigned emax = 0u;
+        for (int64_t j0 = threadIdx.x; j0 < S; j0 += (int64_t)blockDim.x * WIN_BATCH) {
+            double v[WIN_BATCH];
+#pragma unroll
+            for (int k = 0; k < WIN_BATCH; ++k) {
+                const int64_t j = j0 + (int64_t)k * blockDim.x;
+                v[k] = j < S ? __ldcs(in.at[a] + j * stride) : 0.0;
+            }
+#pragma unroll
+            for (int k = 0; k < WIN_BATCH; ++k) {
+                const unsigned eb = ((unsigned)__double2hiint(v[k]) >> 20) & 0x7ffu;
+                if (eb != 0x7ffu && eb > emax) emax = eb;
+            }
+        }
+        const unsigned m = __reduce_max_sync(0xffffffffu, emax);
+        if ((threadIdx.x & 31) == 0 && m) atomicMax(&acc.fxexp[a], m);
+    }
+    // coarse histogram of the sampled rows
+    if (work && !P.full) {
+        for (int64_t j0 = threadIdx.x; j0 < S; j0 += (int64_t)blockDim.x * WIN_BATCH) {
+            double x[WIN_BATCH][3];
+#pragma unroll
+            for (int k = 0; k < WIN_BATCH; ++k) {
+                const int64_t j = j0 + (int64_t)k * blockDim.x;
+#pragma unroll
+                for (int d = 0; d < 3; ++d) x[k][d] = (d < D && j < S) ? __ldcs(in.ax[d] + j * stride) : 0.0;
+            }
+#pragma unroll
+            for (int k = 0; k < WIN_BATCH; ++k) {
+                const int64_t j = j0 + (int64_t)k * blockDim.x;
+                bool inside = j < S;
+                int c = 0, mul = 1;
+#pragma unroll
+                for (int d = 0; d < 3; ++d) {
+                    if (d >= D) break;
+                    inside = inside && (G.lo[d] <= x[k][d]) && (x[k][d] <= G.hi[d]);
+                    const int kd = min(floor_nonneg(__dmul_rn(__dsub_rn(x[k][d], G.lo[d]), G.scale[d])), G.res[d] - 1);
+                    c += (kd / P.cs[d]) * mul;
+                    mul *= P.nc[d];
+                }
+                if (inside) atomicAdd(&hist[c], 1u);
+            }
+        }
+    }
+    __syncthreads();
+    window_pick(g, G, P, acc, hist, best);
+}
+
+__global__ void __launch_bounds__(PREP_THREADS) k_prep(Geom g, Inputs in, Accum acc, int wcap, int choose) {
+    if (choose && blockIdx.x == 0) {  // manual bounds: the window needs no other input
+        window_choose(g, in, acc, wcap);
+        return;
+    }
+    const int zb = choose ? (int)blockIdx.x - 1 : (int)blockIdx.x, nzb = choose ? gridDim.x - 1 : gridDim.x;
+    const uint64_t nb = acc.nbins;
+    const int64_t stride = (int64_t)nzb * blockDim.x;
+    const int64_t t0 = (int64_t)zb * blockDim.x + threadIdx.x;
+    for (int64_t i = t0; i < (int64_t)nb + 2; i += stride) acc.count[i] = 0ull;
+    for (int64_t i = t0; i < (int64_t)(nb * acc.nsum); i += stride) acc.sum[i] = 0.0;
+    const ulonglong2 ident = make_ulonglong2(~0ull, ~0ull);
+    for (int64_t i = t0; i < (int64_t)(nb * acc.nmm); i += stride) ((ulonglong2 *)acc.mm)[i] = ident;
+    if (t0 < 2 * g.ndim) acc.bounds[t0] = ~0ull;
+}
+
+__global__ void __launch_bounds__(PREP_THREADS) k_window(Geom g, Inputs in, Accum acc, int wcap) {
+    window_choose(g, in, acc, wcap);
+}
+
+cudaError_t launch_init(const Geom &g, const Inputs &in, const Accum &acc, int wcap, bool choose_window,
+                        cudaStream_t s) {
+    const int64_t work = (int64_t)acc.nbins * (1 + acc.nsum + acc.nmm);
+    int64_t blocks = (work / 2 + PREP_THREADS - 1) / PREP_THREADS;
+    if (blocks < 16) blocks = 16;
+    if (blocks > 148 * 4) blocks = 148 * 4;
+    k_prep<<<(unsigned)blocks + (choose_window ? 1 : 0), PREP_THREADS, 0, s>>>(g, in, acc, wcap, choose_window ? 1 : 0);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_window(const Geom &g, const Inputs &in, const Accum &acc, int wcap, cudaStream_t s) {
+    k_window<<<1, PREP_THREADS, 0, s>>>(g, in, acc, wcap);
     return cudaGetLastError();
 }
 
@@ -103,229 +212,34 @@ cudaError_t launch_bounds(const Geom &g, const Inputs &in, const Accum &acc, con
     return cudaGetLastError();
 }
 
-// ---------------------------------------------------------------- window
-// Chooses the extents (product <= wcap) and the origin of the box of bins
-// that each binning CTA privatises in shared memory.  The origin maximises
-// the number of sampled rows inside the box (coarse histogram + summed-area
-// table).  Only performance depends on this choice, never results.
-//   k_window_sample  WIN_SAMPLE_CTAS CTAs: strided sample -> coarse histogram
-//   k_window_pick    1 CTA: summed-area table, best box, writes acc.window
-constexpr int WIN_THREADS = 1024;
-constexpr int WIN_SAMPLE_CTAS = 64;
-constexpr int WIN_SAMPLE_THREADS = 256;
-constexpr int WIN_PER_THREAD = 4;
-constexpr int WIN_SAMPLES = WIN_SAMPLE_CTAS * WIN_SAMPLE_THREADS * WIN_PER_THREAD;  // 65536
-constexpr int WIN_CELLS = 4096;
-
-struct WinPlan {
-    int e[3], cs[3], nc[3];
-    bool full, skip;
-};
-
-__device__ __forceinline__ WinPlan window_plan(const DGeom &G, int D, int wcap) {
-    WinPlan P;
-    long long total = (long long)G.res[0] * G.res[1] * G.res[2];
-    P.skip = !G.ok || wcap <= 0;
-    P.full = !P.skip && total <= wcap;
-    for (int d = 0; d < 3; ++d) P.e[d] = P.full ? G.res[d] : 1;
-    if (!P.full && !P.skip) {
-        const int *res = G.res;
-        if (D == 1) {
-            P.e[0] = min(res[0], wcap);
-        } else if (D == 2) {
-            int s = (int)floor(sqrt((double)wcap));
-            P.e[0] = min(res[0], max(1, s));
-            P.e[1] = min(res[1], wcap / P.e[0]);
-            if (P.e[1] == res[1]) P.e[0] = min(res[0], wcap / res[1]);
-        } else {
-            int c = (int)floor(cbrt((double)wcap));
-            P.e[0] = min(res[0], max(1, c));
-            P.e[1] = min(res[1], max(1, c));
-            P.e[2] = min(res[2], wcap / (P.e[0] * P.e[1]));
-            if (P.e[2] == res[2]) {
-                int s = (int)floor(sqrt((double)(wcap / res[2])));
-                P.e[0] = min(res[0], max(1, s));
-                P.e[1] = min(res[1], wcap / (res[2] * P.e[0]));
-            }
-        }
-    }
-    int ncmax = D == 1 ? WIN_CELLS : (D == 2 ? 64 : 16);
-    for (int d = 0; d < 3; ++d) {
-        P.cs[d] = (G.res[d] + ncmax - 1) / ncmax;
-        P.nc[d] = (G.res[d] + P.cs[d] - 1) / P.cs[d];
-    }
-    return P;
-}
-
-__global__ void __launch_bounds__(WIN_SAMPLE_THREADS) k_window_sample(Geom g, Inputs in, Accum acc, int wcap) {
-    const int D = g.ndim;
-    DGeom G = load_geom(g, acc.bounds);
-    WinPlan P = window_plan(G, D, wcap);
-    if (P.skip || in.n == 0) return;
-    const int64_t S = in.n < WIN_SAMPLES ? in.n : WIN_SAMPLES;
-    const int64_t stride = in.n / S;
-    const int tid = blockIdx.x * WIN_SAMPLE_THREADS + threadIdx.x;
-    // magnitude of the summed attributes: max biased exponent over the sample
-    // (sets the fixed-point scale of the shared-memory sums; see k_bin)
-    for (int a = 0; a < in.nattr; ++a) {
-        if (!((acc.sum_mask >> a) & 1u)) continue;
-        unsigned emax = 0;
-#pragma unroll
-        for (int k = 0; k < WIN_PER_THREAD; ++k) {
-            int64_t j = tid + (int64_t)k * WIN_SAMPLE_CTAS * WIN_SAMPLE_THREADS;
-            if (j < S) {
-                double v = in.at[a][j * stride];
-                unsigned eb = ((unsigned)__double2hiint(v) >> 20) & 0x7ffu;
-                emax = (eb != 0x7ffu && eb > emax) ? eb : emax;
-            }
-        }
-        for (int o = 16; o > 0; o >>= 1) emax = max(emax, __shfl_xor_sync(0xffffffffu, emax, o));
-        if ((threadIdx.x & 31) == 0 && emax) atomicMax(&acc.fxexp[a], emax);
-    }
-    if (P.full) return;
-    double x[WIN_PER_THREAD][3];
-#pragma unroll
-    for (int k = 0; k < WIN_PER_THREAD; ++k) {  // all loads first: one latency, not four
-        int64_t j = tid + (int64_t)k * WIN_SAMPLE_CTAS * WIN_SAMPLE_THREADS;
-        int64_t row = (j < S ? j : 0) * stride;
-#pragma unroll
-        for (int d = 0; d < 3; ++d) x[k][d] = d < D ? __ldcs(in.ax[d] + row) : 0.0;
-    }
-#pragma unroll
-    for (int k = 0; k < WIN_PER_THREAD; ++k) {
-        int64_t j = tid + (int64_t)k * WIN_SAMPLE_CTAS * WIN_SAMPLE_THREADS;
-        if (j >= S) continue;
-        bool inside = true;
-        int c = 0, mul = 1;
-        for (int d = 0; d < D; ++d) {
-            inside = inside && (G.lo[d] <= x[k][d]) && (x[k][d] <= G.hi[d]);
-            int kd = min(floor_nonneg(__dmul_rn(__dsub_rn(x[k][d], G.lo[d]), G.scale[d])), G.res[d] - 1);
-            c += (kd / P.cs[d]) * mul;
-            mul *= P.nc[d];
-        }
-        if (inside) atomicAdd(&acc.whist[c], 1u);
-    }
-}
-
-__global__ void __launch_bounds__(WIN_THREADS) k_window_pick(Geom g, Accum acc, int wcap) {
-    __shared__ unsigned hist[WIN_CELLS];
-    __shared__ unsigned long long best[WIN_THREADS / 32];
-    const int D = g.ndim;
-    DGeom G = load_geom(g, acc.bounds);
-    WinPlan P = window_plan(G, D, wcap);
-    if (P.skip) {
-        if (threadIdx.x < 6) acc.window[threadIdx.x] = 0;
-        return;
-    }
-    if (P.full) {
-        if (threadIdx.x < 3) {
-            acc.window[threadIdx.x] = 0;
-            acc.window[3 + threadIdx.x] = G.res[threadIdx.x];
-        }
-        return;
-    }
-    const int *nc = P.nc;
-    const int ncell = nc[0] * nc[1] * nc[2];
-    for (int i = threadIdx.x; i < WIN_CELLS; i += blockDim.x) hist[i] = i < ncell ? acc.whist[i] : 0u;
-    __syncthreads();
-    // summed-area table, one axis at a time
-    for (int d = 0; d < D; ++d) {
-        int len = nc[d];
-        int lines = ncell / len;
-        int step = d == 0 ? 1 : (d == 1 ? nc[0] : nc[0] * nc[1]);
-        if (D == 1) {  // Hillis-Steele over up to WIN_CELLS entries
-            for (int off = 1; off < len; off <<= 1) {
-                unsigned v[WIN_CELLS / WIN_THREADS];
-                for (int r = 0; r < WIN_CELLS / WIN_THREADS; ++r) {
-                    int i = threadIdx.x + r * WIN_THREADS;
-                    v[r] = (i < len && i >= off) ? hist[i - off] : 0u;
-                }
-                __syncthreads();
-                for (int r = 0; r < WIN_CELLS / WIN_THREADS; ++r) {
-                    int i = threadIdx.x + r * WIN_THREADS;
-                    if (i < len) hist[i] += v[r];
-                }
-                __syncthreads();
-            }
-        } else {
-            for (int ln = threadIdx.x; ln < lines; ln += blockDim.x) {
-                int base;
-                if (d == 0) base = ln * nc[0];
-                else if (d == 1) base = (ln % nc[0]) + (ln / nc[0]) * nc[0] * nc[1];
-                else base = ln;
-                unsigned acc_v = 0;
-                for (int i = 0; i < len; ++i) {
-                    acc_v += hist[base + i * step];
-                    hist[base + i * step] = acc_v;
-                }
-            }
-            __syncthreads();
-        }
-    }
-    // candidate boxes on the coarse lattice
-    int wc[3], np[3];
-    for (int d = 0; d < 3; ++d) {
-        wc[d] = d < D ? max(1, P.e[d] / P.cs[d]) : 1;
-        np[d] = nc[d] - wc[d] + 1;
-    }
-    auto sat = [&](int i0, int i1, int i2) -> long long {
-        if (i0 < 0 || i1 < 0 || i2 < 0) return 0;
-        return hist[i0 + nc[0] * (i1 + nc[1] * i2)];
-    };
-    unsigned long long mybest = 0;  // (count << 32) | (0xffffffff - candidate): ties -> lowest index
-    int ncand = np[0] * np[1] * np[2];
-    for (int c = threadIdx.x; c < ncand; c += blockDim.x) {
-        int o0 = c % np[0], o1 = (c / np[0]) % np[1], o2 = c / (np[0] * np[1]);
-        int a0 = o0 - 1, a1 = o1 - 1, a2 = o2 - 1;
-        int b0 = o0 + wc[0] - 1, b1 = o1 + wc[1] - 1, b2 = o2 + wc[2] - 1;
-        long long v = sat(b0, b1, b2) - sat(a0, b1, b2) - sat(b0, a1, b2) - sat(b0, b1, a2) + sat(a0, a1, b2) +
-                      sat(a0, b1, a2) + sat(b0, a1, a2) - sat(a0, a1, a2);
-        unsigned long long key = ((unsigned long long)v << 32) | (0xffffffffull - (unsigned)c);
-        mybest = key > mybest ? key : mybest;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        unsigned long long w = __shfl_xor_sync(0xffffffffu, mybest, o);
-        mybest = w > mybest ? w : mybest;
-    }
-    if ((threadIdx.x & 31) == 0) best[threadIdx.x >> 5] = mybest;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned long long b = 0;
-        for (int i = 0; i < WIN_THREADS / 32; ++i) b = best[i] > b ? best[i] : b;
-        int c = (int)(0xffffffffull - (b & 0xffffffffull));
-        int o[3] = {c % np[0], (c / np[0]) % np[1], c / (np[0] * np[1])};
-        for (int d = 0; d < 3; ++d) {
-            int org = o[d] * P.cs[d];
-            if (org + P.e[d] > G.res[d]) org = G.res[d] - P.e[d];
-            acc.window[d] = org;
-            acc.window[3 + d] = P.e[d];
-        }
-    }
-}
-
-cudaError_t launch_window(const Geom &g, const Inputs &in, const Accum &acc, int wcap, cudaStream_t s) {
-    k_window_sample<<<WIN_SAMPLE_CTAS, WIN_SAMPLE_THREADS, 0, s>>>(g, in, acc, wcap);
-    k_window_pick<<<1, WIN_THREADS, 0, s>>>(g, acc, wcap);
-    return cudaGetLastError();
-}
-
 // ---------------------------------------------------------------- finalize [a7]
 __global__ void k_finalize(Geom g, Accum acc, Meta *meta, int variant) {
     DGeom G = load_geom(g, acc.bounds);
     const uint64_t nb = acc.nbins;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (G.ok) {
+    if (G.ok && acc.nsum <= 1 && acc.nmm <= 1) {
+        // common case: issue the bin's loads together (one latency, not three)
         for (int64_t b = t0; b < (int64_t)nb; b += stride) {
-            unsigned long long cnt = acc.count[b];
-            double dc = (double)cnt;
+            const unsigned long long cnt = acc.count[b];
+            const double sm = acc.nsum ? acc.sum[b] : 0.0;
+            const ulonglong2 m = acc.nmm ? ((const ulonglong2 *)acc.mm)[b] : make_ulonglong2(0ull, 0ull);
+            if (acc.nsum) acc.oavg[b] = cnt ? __ddiv_rn(sm, (double)cnt) : __longlong_as_double(0x7ff8000000000000ll);
+            if (acc.nmm) {
+                acc.omin[b] = cnt ? dec_total(m.x) : __longlong_as_double(0x7ff0000000000000ll);
+                acc.omax[b] = cnt ? dec_total(~m.y) : __longlong_as_double((long long)0xfff0000000000000ull);
+            }
+        }
+    } else if (G.ok) {
+        for (int64_t b = t0; b < (int64_t)nb; b += stride) {
+            const unsigned long long cnt = acc.count[b];
+            const double dc = (double)cnt;
             for (int s = 0; s < acc.nsum; ++s) {
-                double sm = acc.sum[(uint64_t)s * nb + b];
+                const double sm = acc.sum[(uint64_t)s * nb + b];
                 acc.oavg[(uint64_t)s * nb + b] = cnt ? __ddiv_rn(sm, dc) : __longlong_as_double(0x7ff8000000000000ll);
             }
             for (int s = 0; s < acc.nmm; ++s) {
-                ulonglong2 m = ((const ulonglong2 *)acc.mm)[(uint64_t)s * nb + b];
+                const ulonglong2 m = ((const ulonglong2 *)acc.mm)[(uint64_t)s * nb + b];
                 acc.omin[(uint64_t)s * nb + b] = cnt ? dec_total(m.x) : __longlong_as_double(0x7ff0000000000000ll);
                 acc.omax[(uint64_t)s * nb + b] = cnt ? dec_total(~m.y) : __longlong_as_double((long long)0xfff0000000000000ull);
             }
@@ -342,9 +256,9 @@ __global__ void k_finalize(Geom g, Accum acc, Meta *meta, int variant) {
             meta->window[d] = acc.window[d];
             meta->window[3 + d] = acc.window[3 + d];
         }
-        __threadfence_system();
-        meta->done = 1;
+        meta->done = 1;  // device memory; the host copies it on demand (bin_wait)
     }
+    if (t0 < BIN_MAX_ATTR) acc.fxexp[t0] = 0u;  // for the next execute's sample on this slot
 }
 
 cudaError_t launch_finalize(const Geom &g, const Accum &acc, Meta *meta_dev, int64_t n_rows_local, int variant,
