@@ -134,6 +134,20 @@ cudaError_t launch_finalize(const Geom &g, const Accum &acc, Meta *meta_dev, int
 int window_bytes_per_bin(const Accum &acc);
 
 
+// fused NVLink combine + finalize (combine_peer.cu)
+constexpr int PEER_MAX = 16;  // ranks on the node (barrier words hold up to 64)
+struct PeerSet {
+    Accum me;  // this rank's slot (local pointers)
+    unsigned long long *count[PEER_MAX];  // every rank's slot arrays, mapped here (CUDA IPC)
+    double *sum[PEER_MAX];
+    unsigned long long *mm[PEER_MAX];
+    double *omin[PEER_MAX], *omax[PEER_MAX], *oavg[PEER_MAX];
+    unsigned long long *flags[PEER_MAX];  // every rank's barrier words [A: 0..63][B: 64..127]
+    unsigned *ctas_done;                  // this rank's last-CTA counter
+};
+cudaError_t launch_combine_peer(const Geom &g, const PeerSet &ps, int rank, int nranks, unsigned long long epoch,
+                                Meta *meta, int variant, int deterministic, int sms, cudaStream_t s);
+
 // deterministic mode (sort-based, bit-exact vs the sequential oracle)
 struct DetScratch {
     uint32_t *keys = nullptr, *keys_alt = nullptr;   // bin index per row (or ~0 for outside)

@@ -6,6 +6,7 @@
 #include <math.h>
 #include <nccl.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <vector>
@@ -20,6 +21,8 @@ enum { EV_STAGE = 0, EV_INIT0, EV_INIT1, EV_BOUNDS1, EV_WINDOW1, EV_BIN1, EV_COM
 
 struct Slot {
     Accum acc{};
+    unsigned char *base = nullptr;  // the slot's single device allocation (IPC-exported in peer mode)
+    PeerSet peers{};
     Meta *meta_h = nullptr, *meta_d = nullptr;
     cudaEvent_t done = nullptr, released = nullptr;
     cudaEvent_t ev[EV_N] = {};
@@ -62,6 +65,10 @@ struct bin_handle {
     bin_profile_t pacc{};
     cudaStream_t last = nullptr;
     DetScratch det;
+    bool peer = false;                       // fused NVLink combine (combine_peer.cu) instead of NCCL
+    unsigned long long *flags = nullptr;     // this rank's barrier words (IPC-exported)
+    unsigned *ctas_done = nullptr;
+    std::vector<void *> opened;              // peer mappings to close at finalize
     double *gather = nullptr;  // deterministic multi-rank: nranks x nsum x nbins partial sums
     size_t gather_bytes = 0;
     bool finalized = false;
@@ -102,6 +109,7 @@ static int alloc_slot(bin_handle *h, Slot &s) {
     size_t total = o_meta + al(sizeof(Meta));
     unsigned char *base = nullptr;
     cudaError_t e = cudaMalloc(&base, total);
+    s.base = base;
     if (e != cudaSuccess) {
         cudaGetLastError();
         return set_error(BIN_ENOMEM, "bin_init: %zu bytes of bin arrays on device %d", total, h->device);
@@ -202,6 +210,106 @@ int bin_nccl_unique_id(void *out128) {
     return BIN_OK;
 }
 
+// Peer mode: map every rank's slot allocations and barrier words into this
+// process with CUDA IPC (handles exchanged through an NCCL all-gather), so the
+// combine + finalize can run as one kernel over NVLink.  All ranks must be on
+// distinct GPUs of one node; every rank must succeed, else all use NCCL.
+static bool setup_peer(bin_handle *h) {
+    const int R = h->nranks, r = h->rank;
+    if (R > PEER_MAX) return false;
+    const char *env = getenv("DATABIN_COMBINE");
+    if (env && strcmp(env, "nccl") == 0) return false;
+    struct Rec {
+        cudaIpcMemHandle_t slot[2], flags;
+        char uuid[16];
+        int ok;
+    };
+    Rec mine;
+    memset(&mine, 0, sizeof mine);
+    mine.ok = 1;
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, h->device) != cudaSuccess) mine.ok = 0;
+    else memcpy(mine.uuid, &prop.uuid, 16);
+    if (cudaMalloc(&h->flags, 128 * sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMemset(h->flags, 0, 128 * sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMalloc(&h->ctas_done, 64) != cudaSuccess || cudaMemset(h->ctas_done, 0, 64) != cudaSuccess)
+        mine.ok = 0;
+    for (int k = 0; k < 2 && mine.ok; ++k)
+        if (cudaIpcGetMemHandle(&mine.slot[k], h->slot[k].base) != cudaSuccess) mine.ok = 0;
+    if (mine.ok && cudaIpcGetMemHandle(&mine.flags, h->flags) != cudaSuccess) mine.ok = 0;
+    cudaGetLastError();
+    // all-gather the records through NCCL (device buffers)
+    const size_t rb = (sizeof(Rec) + 15) & ~(size_t)15;
+    unsigned char *dbuf = nullptr;
+    std::vector<unsigned char> all(rb * R);
+    bool ok = cudaMalloc(&dbuf, rb * (R + 1)) == cudaSuccess;
+    if (ok) ok = cudaMemcpy(dbuf + rb * R, &mine, sizeof mine, cudaMemcpyHostToDevice) == cudaSuccess;
+    if (ok) ok = ncclAllGather(dbuf + rb * R, dbuf, rb, ncclUint8, h->comm, h->side) == ncclSuccess;
+    if (ok) ok = cudaStreamSynchronize(h->side) == cudaSuccess;
+    if (ok) ok = cudaMemcpy(all.data(), dbuf, rb * R, cudaMemcpyDeviceToHost) == cudaSuccess;
+    if (dbuf) cudaFree(dbuf);
+    cudaGetLastError();
+    if (!ok) return false;  // NCCL itself is broken; bin_init reports it on first use
+    std::vector<Rec> rec(R);
+    for (int p = 0; p < R; ++p) memcpy(&rec[p], all.data() + rb * p, sizeof(Rec));
+    bool good = true;
+    for (int p = 0; p < R; ++p) {
+        good = good && rec[p].ok;
+        for (int q = 0; q < p; ++q) good = good && memcmp(rec[p].uuid, rec[q].uuid, 16) != 0;  // one rank per GPU
+    }
+    // open the peers' allocations
+    unsigned char *slot_base[PEER_MAX][2] = {};
+    unsigned long long *flags[PEER_MAX] = {};
+    for (int p = 0; p < R && good; ++p) {
+        if (p == r) {
+            slot_base[p][0] = h->slot[0].base;
+            slot_base[p][1] = h->slot[1].base;
+            flags[p] = h->flags;
+            continue;
+        }
+        void *ptr = nullptr;
+        for (int k = 0; k < 2 && good; ++k) {
+            if (cudaIpcOpenMemHandle(&ptr, rec[p].slot[k], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) good = false;
+            else h->opened.push_back(ptr), slot_base[p][k] = (unsigned char *)ptr;
+        }
+        if (good && cudaIpcOpenMemHandle(&ptr, rec[p].flags, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) good = false;
+        else if (good) h->opened.push_back(ptr), flags[p] = (unsigned long long *)ptr;
+    }
+    cudaGetLastError();
+    // every rank must agree
+    int *dflag = nullptr;
+    int agree = good ? 1 : 0;
+    if (cudaMalloc(&dflag, sizeof(int)) == cudaSuccess &&
+        cudaMemcpy(dflag, &agree, sizeof(int), cudaMemcpyHostToDevice) == cudaSuccess &&
+        ncclAllReduce(dflag, dflag, 1, ncclInt32, ncclMin, h->comm, h->side) == ncclSuccess &&
+        cudaStreamSynchronize(h->side) == cudaSuccess)
+        cudaMemcpy(&agree, dflag, sizeof(int), cudaMemcpyDeviceToHost);
+    else
+        agree = 0;
+    if (dflag) cudaFree(dflag);
+    cudaGetLastError();
+    if (!agree) return false;
+    for (int k = 0; k < 2; ++k) {
+        Slot &S = h->slot[k];
+        PeerSet &ps = S.peers;
+        ps.me = S.acc;
+        ps.ctas_done = h->ctas_done + k;
+        auto rel = [&](const void *local, int p) {
+            return slot_base[p][k] + ((const unsigned char *)local - S.base);
+        };
+        for (int p = 0; p < R; ++p) {
+            ps.count[p] = (unsigned long long *)rel(S.acc.count, p);
+            ps.sum[p] = (double *)rel(S.acc.sum, p);
+            ps.mm[p] = (unsigned long long *)rel(S.acc.mm, p);
+            ps.omin[p] = (double *)rel(S.acc.omin, p);
+            ps.omax[p] = (double *)rel(S.acc.omax, p);
+            ps.oavg[p] = (double *)rel(S.acc.oavg, p);
+            ps.flags[p] = flags[p];
+        }
+    }
+    return true;
+}
+
 int bin_init(const bin_spec_t *spec, const bin_placement_t *place, const bin_comm_t *comm, bin_handle_t **out) {
     if (!spec || !out) return set_error(BIN_EINVAL, "bin_init: NULL spec/out");
     *out = nullptr;
@@ -281,6 +389,7 @@ int bin_init(const bin_spec_t *spec, const bin_placement_t *place, const bin_com
             h->comm = nullptr;
             return fail(nccl_error(r, "ncclCommInitRank"));
         }
+        h->peer = setup_peer(h);
     }
     *out = h;
     return BIN_OK;
@@ -454,6 +563,16 @@ int bin_execute(bin_handle_t *h, bin_array_t *const *axes, int32_t naxes, bin_ar
         variant = ((uint64_t)h->wcap >= h->nbins ? 2 : 1) | (fast ? 16 : 0);
     }
     if ((rc = rec(EV_BIN1))) return rc;
+    // ---- a6 + a7 fused over NVLink peer memory (one kernel), or NCCL + finalize
+    if (h->peer) {
+        if ((rc = rec(EV_COMBINE1))) return rc;
+        if ((e = launch_combine_peer(geom, S.peers, h->rank, h->nranks, t, S.meta_d, variant | 32,
+                                     h->spec.deterministic, h->lc.sms, s)) != cudaSuccess)
+            return cuda_error(e, "peer combine kernel");
+        S.launches++;
+        S.variant = variant | 32;
+        if ((rc = rec(EV_FINAL1))) return rc;
+    } else {
     // ---- a6: cross-rank combine over NVLink (one NCCL group)
     if (h->comm) {
         const uint64_t B = h->nbins;
@@ -480,6 +599,7 @@ int bin_execute(bin_handle_t *h, bin_array_t *const *axes, int32_t naxes, bin_ar
     S.launches++;
     S.variant = variant;
     if ((rc = rec(EV_FINAL1))) return rc;
+    }
     DB_CUDA(cudaEventRecord(S.done, s));
     if (!staged_any) DB_CUDA(cudaEventRecord(S.released, s));
     S.prof_pending = h->prof;
@@ -548,6 +668,8 @@ int bin_wait(bin_handle_t *h, uint64_t ticket) {
     int rc = fetch_meta(h, *S);
     if (rc) return rc;
     accumulate_profile(h, *S);
+    if (S->meta_h->status == BIN_ENCCL)
+        return set_error(BIN_ENCCL, "peer combine: a rank did not reach the NVLink barrier within ~2 s");
     if (S->meta_h->status == BIN_EDEGENERATE)
         return set_error(BIN_EDEGENERATE, "auto bounds: no finite rows in total, or an infinite/unrecoverable axis");
     return BIN_OK;
@@ -618,6 +740,12 @@ int bin_finalize(bin_handle_t *h) {
                 if (e != cudaSuccess && rc == BIN_OK) rc = cuda_error(e, "bin_finalize");
             }
         if (h->side) cudaStreamSynchronize(h->side);
+        for (void *p : h->opened) cudaIpcCloseMemHandle(p);
+        h->opened.clear();
+        if (h->flags) cudaFree(h->flags);
+        if (h->ctas_done) cudaFree(h->ctas_done);
+        h->flags = nullptr;
+        h->ctas_done = nullptr;
         if (h->comm) {
             ncclCommDestroy(h->comm);
             h->comm = nullptr;

@@ -10,6 +10,13 @@ python -c "
 import json
 for f in ['gpurun_out/bench_n$N.json','gpurun_out/bench_n${N}_weak.json']:
     try:
-        d=json.load(open(f)); print(f, round(d['value']/1e9,1), 'G/s', d['ms_per_step'], d['phases_ms_per_step'])
+        d=json.loads([l for l in open(f) if l.startswith("{")][-1]); print(f, round(d['value']/1e9,1), 'G/s', d['ms_per_step'], d['phases_ms_per_step'])
     except Exception as e: print(f, 'ERR', e)
 "
+if [ "${AB_NCCL:-0}" = "1" ]; then
+DATABIN_COMBINE=nccl timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29514 bench.py --gpus $N --steps 100 --warmup 5 --no-cpu-baseline --no-e2e > gpurun_out/bench_n${N}_nccl.json 2>> gpurun_out/bench_n$N.err; echo bench_nccl=$?
+python -c "
+import json
+d=json.loads([l for l in open('gpurun_out/bench_n${N}_nccl.json') if l.startswith('{')][-1]); print('nccl combine', round(d['value']/1e9,1), 'G/s', d['ms_per_step'], d['phases_ms_per_step'])
+"
+fi
