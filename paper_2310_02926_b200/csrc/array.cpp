@@ -308,6 +308,10 @@ int bin_array_get_accessible(bin_array_t *a, int32_t device, bin_stream_t stream
             if (e != cudaSuccess) rc = cuda_error(e, "get_accessible H2D");
         } else {
             DeviceGuard g(device);
+            int can = 0;  // NVLink direct access (else the copy stages through the host)
+            if (cudaDeviceCanAccessPeer(&can, device, a->device) == cudaSuccess && can)
+                cudaDeviceEnablePeerAccess(a->device, 0);
+            cudaGetLastError();
             cudaError_t e = cudaMemcpyPeerAsync(v->ptr, device, a->ptr, a->device, bytes, s);
             if (e != cudaSuccess) rc = cuda_error(e, "get_accessible peer copy");
         }

@@ -111,9 +111,13 @@ __device__ __forceinline__ uint32_t fast_row(const FastCtx<D> &c, const double (
 // One queued item as fire-and-forget L2 reductions.  A QK_GLOBAL item from
 // inside the window (value outside the fixed range) carries sum + min/max but
 // its count is already in shared memory -> the low bit of `kind` picks count.
+// `gf` (the CTA's window covers under half its rows, e.g. uniform data): the
+// global rows' min/max first read the slot pair from L2 and reduce only when
+// they improve it (stale reads are safe: the slots only decrease), which turns
+// two L2 atomics per global row into one load for all but the first rows.
 template <int A, int SM, int MM>
 __device__ __forceinline__ void fast_exec(uint32_t tag, double v, unsigned long long *count, double *sum,
-                                          ulonglong2 *mm) {
+                                          ulonglong2 *mm, bool gf) {
     constexpr bool HS = A == 1 && SM == 1, HM = A == 1 && MM == 1;
     const uint32_t kind = tag >> 29, b = tag & QBIN;
     if (kind & QK_GLOBAL) {
@@ -121,8 +125,10 @@ __device__ __forceinline__ void fast_exec(uint32_t tag, double v, unsigned long 
         if (HS) atomicAdd(&sum[b], v);
         if (HM) {
             const unsigned long long e = enc_total(v);
-            atomicMin(&mm[b].x, e);
-            atomicMin(&mm[b].y, ~e);
+            ulonglong2 cur = make_ulonglong2(~0ull, ~0ull);
+            if (gf) cur = __ldcg(&mm[b]);
+            if (e < cur.x) atomicMin(&mm[b].x, e);
+            if (~e < cur.y) atomicMin(&mm[b].y, ~e);
         }
     } else if (HM) {
         const unsigned long long e = enc_total(v);
@@ -133,7 +139,7 @@ __device__ __forceinline__ void fast_exec(uint32_t tag, double v, unsigned long 
 
 template <int A, int SM, int MM>
 __device__ __forceinline__ void fast_push(uint32_t qb, uint32_t &qn, uint32_t tag, double v, unsigned lane,
-                                          unsigned long long *count, double *sum, ulonglong2 *mm) {
+                                          unsigned long long *count, double *sum, ulonglong2 *mm, bool gf) {
     const unsigned m = __ballot_sync(0xffffffffu, tag != 0);
     if (m == 0) return;
     double *vals = (double *)&f_dsm[qb + QCAP];
@@ -160,7 +166,7 @@ __device__ __forceinline__ void fast_push(uint32_t qb, uint32_t &qn, uint32_t ta
             vals[lane] = v2;
         }
         qn = rest;
-        fast_exec<A, SM, MM>(t, vv, count, sum, mm);
+        fast_exec<A, SM, MM>(t, vv, count, sum, mm, gf);
         __syncwarp();
     }
 }
@@ -226,8 +232,8 @@ __device__ __forceinline__ void fast_choose_window(const DGeom G, const WinPlan 
     __syncthreads();
     if (hist) {
         pick_box<D>(P, G.res[0], G.res[1], G.res[2], f_dsm, s_best, s_origin);
-    } else if (threadIdx.x < 3) {
-        s_origin[threadIdx.x] = 0;
+    } else if (threadIdx.x < 4) {
+        s_origin[threadIdx.x] = threadIdx.x == 3 && P.skip ? 1 : 0;
     }
     __syncthreads();  // the histogram scratch becomes the window after this
 }
@@ -237,7 +243,7 @@ __global__ void __launch_bounds__(FAST_THREADS, 1)
     k_bin_fast(Geom g, Inputs in, Accum acc, uint32_t npairs, int head, int wcap) {
     constexpr bool HS = A == 1 && SM == 1, HM = A == 1 && MM == 1;
     __shared__ unsigned long long s_best[FAST_THREADS / 32];
-    __shared__ int s_origin[3];
+    __shared__ int s_origin[4];
     __shared__ unsigned s_exp;
     FastCtx<D> c;
     unsigned long long *const count = acc.count;
@@ -280,6 +286,11 @@ __global__ void __launch_bounds__(FAST_THREADS, 1)
         }
     }
     c.fx = fx_param(HS ? s_exp : 0u);
+#ifdef BIN_GF_OFF
+    const bool gf = false;
+#else
+    const bool gf = s_origin[3] != 0;
+#endif
     double2 bx[D], bv = make_double2(0.0, 0.0);
     if (p0 < npairs) {
 #pragma unroll
@@ -313,11 +324,11 @@ __global__ void __launch_bounds__(FAST_THREADS, 1)
 #pragma unroll
         for (int d = 0; d < D; ++d) x[d] = bx[d].x;
         uint32_t t0 = fast_row<D, A, SM, MM>(c, x, bv.x, valid, n_in);
-        fast_push<A, SM, MM>(qb, qn, t0, bv.x, lane, count, sum, mm);
+        fast_push<A, SM, MM>(qb, qn, t0, bv.x, lane, count, sum, mm, gf);
 #pragma unroll
         for (int d = 0; d < D; ++d) x[d] = bx[d].y;
         uint32_t t1 = fast_row<D, A, SM, MM>(c, x, bv.y, valid, n_in);
-        fast_push<A, SM, MM>(qb, qn, t1, bv.y, lane, count, sum, mm);
+        fast_push<A, SM, MM>(qb, qn, t1, bv.y, lane, count, sum, mm, gf);
         rows += valid ? 2u : 0u;
 #pragma unroll
         for (int d = 0; d < D; ++d) bx[d] = nx[d];
@@ -333,10 +344,10 @@ __global__ void __launch_bounds__(FAST_THREADS, 1)
         if (A == 1 && r >= 0) v = in.at[0][r];
         const uint32_t t = fast_row<D, A, SM, MM>(c, x, v, r >= 0, n_in);
         rows += r >= 0 ? 1u : 0u;
-        fast_push<A, SM, MM>(qb, qn, t, v, lane, count, sum, mm);
+        fast_push<A, SM, MM>(qb, qn, t, v, lane, count, sum, mm, gf);
     }
     __syncwarp();
-    if (lane < qn) fast_exec<A, SM, MM>(f_dsm[qb + lane], ((double *)&f_dsm[qb + QCAP])[lane], count, sum, mm);
+    if (lane < qn) fast_exec<A, SM, MM>(f_dsm[qb + lane], ((double *)&f_dsm[qb + QCAP])[lane], count, sum, mm, gf);
 
     unsigned long long in_w = n_in, out_w = rows - n_in;
 #pragma unroll

@@ -319,6 +319,9 @@ __device__ __forceinline__ void pick_box(const WinPlan P, const int res0, const 
             if (org + P.e[d] > res[d]) org = res[d] - P.e[d];
             origin[d] = org;
         }
+        // origin[3]: the box holds under half of the sampled rows inside the
+        // grid (spread-out data: most rows take the global path)
+        origin[3] = (bb >> 32) * 2 < (unsigned long long)hist[ncell - 1] ? 1 : 0;
     }
     __syncthreads();
 }

@@ -52,6 +52,7 @@ struct bin_handle {
     ncclComm_t comm = nullptr;
     cudaStream_t side = nullptr;
     cudaStream_t meta_stream = nullptr;
+    cudaStream_t copy = nullptr;  // staging copies (host, peer, snapshot)
     Slot slot[2];
     uint64_t next_ticket = 1;
     Stage stage[2][BIN_MAX_DIM + BIN_MAX_ATTR];
@@ -359,6 +360,15 @@ int bin_init(const bin_spec_t *spec, const bin_placement_t *place, const bin_com
         return fail(cuda_error(ce, "cudaStreamCreate"));
     if ((ce = cudaStreamCreateWithFlags(&h->meta_stream, cudaStreamNonBlocking)) != cudaSuccess)
         return fail(cuda_error(ce, "cudaStreamCreate"));
+    if ((ce = cudaStreamCreateWithFlags(&h->copy, cudaStreamNonBlocking)) != cudaSuccess)
+        return fail(cuda_error(ce, "cudaStreamCreate"));
+    // direct NVLink access to every other GPU this one can reach (peer copies and
+    // the peer combine); without it cudaMemcpyPeerAsync stages through the host
+    for (int d = 0; d < n_a; ++d) {
+        int can = 0;
+        if (d != dev && cudaDeviceCanAccessPeer(&can, dev, d) == cudaSuccess && can) cudaDeviceEnablePeerAccess(d, 0);
+        cudaGetLastError();  // "already enabled" is fine
+    }
     cudaDeviceGetAttribute(&h->lc.sms, cudaDevAttrMultiProcessorCount, dev);
     cudaDeviceGetAttribute(&h->lc.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     Accum probe{};
@@ -453,54 +463,64 @@ int bin_execute(bin_handle_t *h, bin_array_t *const *axes, int32_t naxes, bin_ar
     h->last = s;
     if (h->prof) DB_CUDA(cudaEventRecord(S.ev[EV_STAGE], s));
 
-    // ---- a1: resolve input views on the analysis device
+    // ---- a1: resolve input views on the analysis device.  Columns already on
+    // it are read in place (zero copy); the others -- host memory, another GPU
+    // (peer copy over NVLink), or an asynchronous snapshot --
+    // are copied into this slot's staging buffers on the handle's copy stream,
+    // so a snapshot/peer copy overlaps the previous execute's binning.
     Inputs in{};
     in.n = n;
     in.nattr = nattr;
     bool staged_any = false;
+    const bool snapshot = h->place.exec == BIN_EXEC_ASYNC && h->place.async_snapshot;
+    bool stage[BIN_MAX_DIM + BIN_MAX_ATTR];
     for (int i = 0; i < ncols; ++i) {
         bin_array *a = cols[i];
-        bool uva = a->alloc == BIN_ALLOC_CUDA_UVA;
-        bool local = uva || (is_device_memory(a) && a->device == h->device);
-        bool snapshot = h->place.exec == BIN_EXEC_ASYNC && h->place.async_snapshot;
+        const bool local = a->alloc == BIN_ALLOC_CUDA_UVA || (is_device_memory(a) && a->device == h->device);
+        stage[i] = n > 0 && (!local || snapshot);
+        staged_any = staged_any || stage[i];
+    }
+    if (staged_any && S.used) DB_CUDA(cudaStreamWaitEvent(h->copy, S.done, 0));  // staging buffers free again
+    for (int i = 0; i < ncols; ++i) {
+        bin_array *a = cols[i];
         const double *p = (const double *)a->ptr;
+        cudaStream_t consumer = stage[i] ? h->copy : s;
         // order after the producer's pending work on its own stream
-        if (a->stream != s && (a->device >= 0 || a->alloc == BIN_ALLOC_HOST_PINNED)) {
-            int pd = a->device >= 0 ? a->device : h->device;
-            {
-                DeviceGuard g2(pd);
-                cudaEvent_t ev = h->producer_ev[i];
-                if (pd != h->device) {
-                    // events are per device: use a temporary on the producer's device
-                    cudaEvent_t tmp;
-                    DB_CUDA(cudaEventCreateWithFlags(&tmp, cudaEventDisableTiming));
-                    DB_CUDA(cudaEventRecord(tmp, a->stream));
-                    DeviceGuard g3(h->device);
-                    DB_CUDA(cudaStreamWaitEvent(s, tmp, 0));
-                    cudaEventDestroy(tmp);
-                } else {
-                    DB_CUDA(cudaEventRecord(ev, a->stream));
-                    DB_CUDA(cudaStreamWaitEvent(s, ev, 0));
-                }
+        if (a->stream != consumer && (a->device >= 0 || a->alloc == BIN_ALLOC_HOST_PINNED)) {
+            const int pd = a->device >= 0 ? a->device : h->device;
+            DeviceGuard g2(pd);
+            if (pd != h->device) {
+                // events are per device: a temporary on the producer's device
+                cudaEvent_t tmp;
+                DB_CUDA(cudaEventCreateWithFlags(&tmp, cudaEventDisableTiming));
+                DB_CUDA(cudaEventRecord(tmp, a->stream));
+                DeviceGuard g3(h->device);
+                DB_CUDA(cudaStreamWaitEvent(consumer, tmp, 0));
+                cudaEventDestroy(tmp);
+            } else {
+                DB_CUDA(cudaEventRecord(h->producer_ev[i], a->stream));
+                DB_CUDA(cudaStreamWaitEvent(consumer, h->producer_ev[i], 0));
             }
         }
-        if (n > 0 && (!local || snapshot)) {
+        if (stage[i]) {
             void *dst = nullptr;
             int rc = stage_buffer(h, sl, i, (size_t)n * 8, &dst);
             if (rc) return rc;
             if (a->device == -1 || a->alloc == BIN_ALLOC_HOST || a->alloc == BIN_ALLOC_HOST_PINNED)
-                DB_CUDA(cudaMemcpyAsync(dst, a->ptr, (size_t)n * 8, cudaMemcpyHostToDevice, s));
-            else if (a->device != h->device && !uva)
-                DB_CUDA(cudaMemcpyPeerAsync(dst, h->device, a->ptr, a->device, (size_t)n * 8, s));
+                DB_CUDA(cudaMemcpyAsync(dst, a->ptr, (size_t)n * 8, cudaMemcpyHostToDevice, h->copy));
+            else if (a->device != h->device && a->alloc != BIN_ALLOC_CUDA_UVA)
+                DB_CUDA(cudaMemcpyPeerAsync(dst, h->device, a->ptr, a->device, (size_t)n * 8, h->copy));
             else
-                DB_CUDA(cudaMemcpyAsync(dst, a->ptr, (size_t)n * 8, cudaMemcpyDeviceToDevice, s));
+                DB_CUDA(cudaMemcpyAsync(dst, a->ptr, (size_t)n * 8, cudaMemcpyDeviceToDevice, h->copy));
             p = (const double *)dst;
-            staged_any = true;
         }
         if (i < naxes) in.ax[i] = p;
         else in.at[i - naxes] = p;
     }
-    if (staged_any) DB_CUDA(cudaEventRecord(S.released, s));  // inputs copied: producer may overwrite
+    if (staged_any) {  // inputs copied: the producer may overwrite; the analysis may start
+        DB_CUDA(cudaEventRecord(S.released, h->copy));
+        DB_CUDA(cudaStreamWaitEvent(s, S.released, 0));
+    }
 
     Geom geom{};
     geom.ndim = h->spec.ndim;
@@ -768,6 +788,11 @@ int bin_finalize(bin_handle_t *h) {
         }
         if (h->side) cudaStreamDestroy(h->side);
         if (h->meta_stream) cudaStreamDestroy(h->meta_stream);
+        if (h->copy) {
+            cudaStreamSynchronize(h->copy);
+            cudaStreamDestroy(h->copy);
+        }
+        h->copy = nullptr;
         h->side = nullptr;
         h->meta_stream = nullptr;
     }

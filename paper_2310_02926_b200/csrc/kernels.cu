@@ -40,7 +40,7 @@ constexpr int WIN_BATCH = 8;  // sample rows per thread in flight
 // Best box from the coarse histogram in shared memory -> acc.window.
 __device__ void window_pick(const Geom &g, const DGeom &G, const WinPlan &P, const Accum &acc, unsigned *hist,
                             unsigned long long *best) {
-    __shared__ int origin[3];
+    __shared__ int origin[4];
     if (P.skip || P.full) {
         if (threadIdx.x < 3) {
             acc.window[threadIdx.x] = 0;
