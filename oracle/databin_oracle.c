@@ -53,18 +53,26 @@ static int total_order_less(double a, double b)
 /* ---- Automatic bounds ("obtained on the fly by
  * calculating the minimum and maximum of the respective coordinate
  * variables"; readings R3/R4) ----
- * Returns 0 on success, -1 when n == 0 (no min/max exists: degenerate). */
+ * NaN rows do not define bounds (reading R4).  Returns 0 on success, -1 when
+ * an axis has no non-NaN value (n == 0 included: degenerate). */
 int oracle_bounds(int ndim, int64_t n, const double *const *axes,
                   double *lo, double *hi)
 {
     if (n <= 0) return -1;
     for (int d = 0; d < ndim; ++d) {
-        double mn = axes[d][0], mx = axes[d][0];
-        for (int64_t i = 1; i < n; ++i) {
+        int seen = 0;
+        double mn = 0.0, mx = 0.0;
+        for (int64_t i = 0; i < n; ++i) {
             double x = axes[d][i];
+            if (x != x) continue;
+            if (!seen) {
+                mn = mx = x;
+                seen = 1;
+            }
             if (total_order_less(x, mn)) mn = x;
             if (total_order_less(mx, x)) mx = x;
         }
+        if (!seen) return -1;
         lo[d] = mn;
         hi[d] = mx;
     }

@@ -143,6 +143,22 @@ def test_auto_bounds_examples():
     assert r["count"].tolist() == [0, 0, 3, 0]
 
 
+def test_auto_bounds_ignore_nan_rows():
+    # reading R4: NaN rows do not define bounds (and then fall outside the mesh);
+    # numpy's nanmin/nanmax are the independent reference; -0.0 < +0.0 (R6)
+    rng = np.random.default_rng(15)
+    x = rng.uniform(-3, 7, 1000)
+    x[[0, 17, 999]] = np.nan
+    lo, hi = oracle.bounds([x])
+    assert (lo[0], hi[0]) == (np.nanmin(x), np.nanmax(x))
+    lo, hi = oracle.bounds([np.array([np.nan, 0.0, -0.0, np.nan])])
+    assert np.signbit(lo[0]) and not np.signbit(hi[0])
+    with pytest.raises(ValueError):
+        oracle.bounds([np.array([np.nan, np.nan])])
+    r = oracle.databin([x], [np.ones(1000)], [10], bounds_auto=True)
+    assert (r["n_in"], r["n_out"]) == (997, 3)
+
+
 def test_auto_bounds_nothing_outside():
     rng = np.random.default_rng(5)
     for _ in range(20):
