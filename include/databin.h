@@ -152,7 +152,18 @@ typedef struct {
     uint32_t ops[BIN_MAX_ATTR]; /* per attribute: OR of BIN_OP_* (AVG implies SUM) */
     int32_t deterministic;      /* 1: sums bit-identical to the sequential oracle
                                    in partition mode P = nranks (slow; correctness mode) */
+    int32_t route;              /* accumulate route (speed only; results agree within the sum
+                                   tolerance): BIN_ROUTE_AUTO (0, default) picks from a 16,384-row
+                                   sample at the first execute (one host wait) and re-checks it
+                                   asynchronously every 64 executes; BIN_ROUTE_WINDOW: shared-memory
+                                   hot window + L2 reductions (clustered data); BIN_ROUTE_PARTITION:
+                                   rows grouped by bin tile, then accumulated tile by tile in shared
+                                   memory (spread-out data, large meshes).  Ignored when
+                                   deterministic; falls back to the window route when the
+                                   partition plan does not apply (> 4 attributes read, n >= 2^32,
+                                   unaligned columns, > 8192 tiles). */
 } bin_spec_t;
+enum { BIN_ROUTE_AUTO = 0, BIN_ROUTE_WINDOW = 1, BIN_ROUTE_PARTITION = 2 };
 
 /* Execution method + placement (Sec. 3; XML attributes at PAPER.md:426-433). */
 enum { BIN_EXEC_SYNC = 0, BIN_EXEC_ASYNC = 1, BIN_EXEC_PEER = 2 };
@@ -205,7 +216,8 @@ typedef struct {
     int64_t kernel_launches;  /* library kernels launched (all phases) */
     int64_t bin_launches;     /* launches of the accumulate kernel */
     int32_t variant;          /* last accumulate variant (low 4 bits): 1 smem window + L2, 2 smem full grid,
-                                 3 deterministic; +16 when the single-attribute k_bin_fast kernel ran */
+                                 3 deterministic, 4 partition route; +16 when the single-attribute
+                                 k_bin_fast kernel ran, +32 when the NVLink peer combine ran */
     int32_t window[BIN_MAX_DIM]; /* last window extents (bins), 0 = no window */
 } bin_profile_t;
 

@@ -36,7 +36,7 @@ def sources():
 
 
 def headers():
-    return sorted(glob.glob(os.path.join(CSRC, "*.h")) + [os.path.join(ROOT, "include", "databin.h")])
+    return sorted(glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(ROOT, "include", "databin.h")])
 
 
 def stale() -> bool:

@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(FAST_THREADS, 1)
     k_bin_fast(Geom g, Inputs in, Accum acc, uint32_t npairs, int head, int wcap) {
     constexpr bool HS = A == 1 && SM == 1, HM = A == 1 && MM == 1;
     __shared__ unsigned long long s_best[FAST_THREADS / 32];
-    __shared__ int s_origin[4];
+    __shared__ int s_origin[6];
     __shared__ unsigned s_exp;
     FastCtx<D> c;
     unsigned long long *const count = acc.count;

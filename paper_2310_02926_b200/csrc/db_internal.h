@@ -134,6 +134,31 @@ cudaError_t launch_finalize(const Geom &g, const Accum &acc, Meta *meta_dev, int
 int window_bytes_per_bin(const Accum &acc);
 
 
+// partition route (bin_part.cu): rows grouped by tile of Wt bins, then
+// accumulated tile by tile in shared memory
+struct PartArgs {
+    uint32_t *keys;    // [2*npairs + 2] bin index per row slot, ~0u outside
+    uint32_t *cnt;     // [T][C] rows of chunk c in tile t -> exclusive prefix over c
+    uint32_t *tot;     // [T] rows per tile
+    uint32_t *tstart;  // [T + 1] first grouped row of each tile
+    uint32_t *off1;    // [T1][C + 1] rows of super-tile s from chunks < c
+    uint32_t *skey;    // [cap] bin index of the rows grouped by tile
+    double *sval;      // [nl][cap] their attribute values
+    uint32_t *xkey;    // [cap] rows grouped by super-tile (G1 > 1 only)
+    double *xval;      // [nl][cap]
+    uint64_t cap;
+    uint32_t npairs;
+    int32_t head, tail;
+    uint32_t Wt, T, C;  // bins per tile, tiles, chunks (CTAs of P1 and P3)
+    uint32_t G1, T1;    // tiles per super-tile (1: one level), super-tiles
+    int32_t nl;         // attributes read (<= 4) and which
+    int32_t lattr[4];
+};
+bool part_plan(const Inputs &in, const Accum &acc, int ndim, int smem_optin, int sms, PartArgs *pa);
+cudaError_t launch_partition(const Geom &g, const Inputs &in, const Accum &acc, const PartArgs &pa, cudaStream_t s,
+                             int *launches);
+cudaError_t launch_probe(const Geom &g, const Inputs &in, const Accum &acc, int wcap, int32_t *out, cudaStream_t s);
+
 // fused NVLink combine + finalize (combine_peer.cu)
 constexpr int PEER_MAX = 16;  // ranks on the node (barrier words hold up to 64)
 struct PeerSet {

@@ -240,7 +240,8 @@ __device__ __forceinline__ void warp_line_scan(unsigned *h, int base, int step, 
 // Summed-area table of the coarse histogram `hist` (shared memory, nc cells),
 // then the box of wc = e/cs coarse cells with the most samples (ties -> lowest
 // index).  All threads of the CTA take part (blockDim >= 256); the box origin
-// in bins is written to origin[0..2] (shared) and is valid after the return.
+// in bins is written to origin[0..2] (shared, int[6], see the end) and is
+// valid after the return.
 template <int D>
 __device__ __forceinline__ void pick_box(const WinPlan P, const int res0, const int res1, const int res2,
                                          unsigned *hist, unsigned long long *best, int *origin) {
@@ -320,8 +321,11 @@ __device__ __forceinline__ void pick_box(const WinPlan P, const int res0, const 
             origin[d] = org;
         }
         // origin[3]: the box holds under half of the sampled rows inside the
-        // grid (spread-out data: most rows take the global path)
+        // grid (spread-out data: most rows take the global path); origin[4],
+        // origin[5]: sampled rows in the box / inside the grid
         origin[3] = (bb >> 32) * 2 < (unsigned long long)hist[ncell - 1] ? 1 : 0;
+        origin[4] = (int)(bb >> 32);
+        origin[5] = (int)hist[ncell - 1];
     }
     __syncthreads();
 }

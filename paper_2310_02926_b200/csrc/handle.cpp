@@ -72,8 +72,77 @@ struct bin_handle {
     std::vector<void *> opened;              // peer mappings to close at finalize
     double *gather = nullptr;  // deterministic multi-rank: nranks x nsum x nbins partial sums
     size_t gather_bytes = 0;
+    // accumulate route (BIN_ROUTE_*): auto = chosen by the k_probe sample
+    int route = 0;                  // 0 not yet chosen, else BIN_ROUTE_WINDOW / BIN_ROUTE_PARTITION
+    int32_t *probe_d = nullptr;     // k_probe output: window[6] + rows in box, rows inside
+    int32_t *probe_h = nullptr;     // pinned mirror
+    cudaEvent_t probe_ev = nullptr;
+    bool probe_inflight = false;
+    int since_probe = 0;
+    unsigned char *part_base = nullptr;  // partition-route scratch (grown on demand)
+    size_t part_bytes = 0;
     bool finalized = false;
 };
+
+// The window route holds a row in shared memory only if it falls in the CTA's
+// hot window; with less than this fraction of the sampled rows in the best
+// window the partition route (bin_part.cu) moves fewer L2 reductions per row.
+static double route_coverage() {
+    const char *e = getenv("DATABIN_ROUTE_COVERAGE");
+    return e ? atof(e) : 0.5;
+}
+constexpr int ROUTE_REPROBE = 64;  // executes between asynchronous re-checks
+
+static int probe_route(const int32_t *p) {
+    return (p[7] > 0 && (double)p[6] < route_coverage() * (double)p[7]) ? BIN_ROUTE_PARTITION : BIN_ROUTE_WINDOW;
+}
+
+// Carves the partition scratch (256-byte aligned pieces): keys [n+2] |
+// cnt [T*C] | tot [T] | tstart [T+1] | off1 [T1*(C+1)] | skey [n] |
+// sval [nl][n] | (two-level) xkey [n] | xval [nl][n].
+static int ensure_part_scratch(bin_handle *h, int64_t n, PartArgs &pa) {
+    auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    const size_t nv = (size_t)(pa.nl > 0 ? pa.nl : 1);
+    size_t o = 0;
+    const size_t o_keys = o; o += al(((size_t)n + 2) * 4);
+    const size_t o_cnt = o; o += al((size_t)pa.T * pa.C * 4);
+    const size_t o_tot = o; o += al((size_t)pa.T * 4);
+    const size_t o_ts = o; o += al(((size_t)pa.T + 1) * 4);
+    const size_t o_off1 = o; o += al((size_t)pa.T1 * (pa.C + 1) * 4);
+    const size_t o_skey = o; o += al((size_t)n * 4);
+    const size_t o_sval = o; o += al((size_t)n * 8 * nv);
+    const size_t o_xkey = o; if (pa.G1 > 1) o += al((size_t)n * 4);
+    const size_t o_xval = o; if (pa.G1 > 1) o += al((size_t)n * 8 * nv);
+    const size_t total = o;
+    if (total > h->part_bytes) {
+        if (h->part_base) {
+            cudaFree(h->part_base);  // synchronises the device: no execute still uses it
+            count_free((int64_t)h->part_bytes);
+            h->part_base = nullptr;
+            h->part_bytes = 0;
+        }
+        const size_t want = total + total / 8;  // headroom for slowly growing n
+        cudaError_t e = cudaMalloc(&h->part_base, want);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            h->part_base = nullptr;
+            return set_error(BIN_ENOMEM, "partition route: %zu bytes of scratch on device %d", want, h->device);
+        }
+        count_alloc((int64_t)want);
+        h->part_bytes = want;
+    }
+    pa.keys = (uint32_t *)(h->part_base + o_keys);
+    pa.cnt = (uint32_t *)(h->part_base + o_cnt);
+    pa.tot = (uint32_t *)(h->part_base + o_tot);
+    pa.tstart = (uint32_t *)(h->part_base + o_ts);
+    pa.off1 = (uint32_t *)(h->part_base + o_off1);
+    pa.skey = (uint32_t *)(h->part_base + o_skey);
+    pa.sval = (double *)(h->part_base + o_sval);
+    pa.xkey = (uint32_t *)(h->part_base + o_xkey);
+    pa.xval = (double *)(h->part_base + o_xval);
+    pa.cap = (uint64_t)n;
+    return BIN_OK;
+}
 
 static int nccl_error(ncclResult_t r, const char *what) {
     return set_error(BIN_ENCCL, "%s: %s", what, ncclGetErrorString(r));
@@ -161,6 +230,8 @@ static int validate_spec(const bin_spec_t *sp, uint64_t *nbins) {
                 return set_error(BIN_EINVAL, "axis %d: hi - lo overflows", d);
         }
     }
+    if (sp->route < BIN_ROUTE_AUTO || sp->route > BIN_ROUTE_PARTITION)
+        return set_error(BIN_EINVAL, "route %d is not a BIN_ROUTE_* value", sp->route);
     for (int a = 0; a < sp->nattr; ++a)
         if (sp->ops[a] & ~(uint32_t)(BIN_OP_SUM | BIN_OP_MIN | BIN_OP_MAX | BIN_OP_AVG))
             return set_error(BIN_EINVAL, "ops[%d] = 0x%x has unknown bits", a, sp->ops[a]);
@@ -454,6 +525,10 @@ int bin_execute(bin_handle_t *h, bin_array_t *const *axes, int32_t naxes, bin_ar
         accumulate_profile(h, S);
     }
     if (S.used && S.stream != s) DB_CUDA(cudaStreamWaitEvent(s, S.done, 0));
+    {  // the previous execute may run on another stream: scratch (det, partition) is shared
+        Slot &P = h->slot[sl ^ 1];
+        if (P.used && P.stream != s) DB_CUDA(cudaStreamWaitEvent(s, P.done, 0));
+    }
     S.ticket = t;
     S.used = true;
     S.meta_valid = false;
@@ -537,10 +612,26 @@ int bin_execute(bin_handle_t *h, bin_array_t *const *axes, int32_t naxes, bin_ar
     };
     int rc;
     if ((rc = rec(EV_INIT0))) return rc;
+    // ---- route: partition (bin_part.cu) or window; auto follows the last probe
+    PartArgs pa{};
+    const bool part_ok = n > 0 && !h->spec.deterministic && h->spec.route != BIN_ROUTE_WINDOW &&
+                         part_plan(in, S.acc, geom.ndim, h->lc.smem_optin, h->lc.sms, &pa);
+    if (part_ok && h->spec.route == BIN_ROUTE_AUTO && h->probe_inflight) {
+        cudaError_t q = cudaEventQuery(h->probe_ev);
+        if (q == cudaSuccess) {
+            h->route = probe_route(h->probe_h);
+            h->probe_inflight = false;
+        } else if (q == cudaErrorNotReady) {
+            cudaGetLastError();
+        } else {
+            return cuda_error(q, "route probe");
+        }
+    }
+    bool part = part_ok && (h->spec.route == BIN_ROUTE_PARTITION || h->route == BIN_ROUTE_PARTITION);
     // ---- a3: accumulator identities (+ the window choice when the bounds are manual
     // and the general kernel will run; k_bin_fast chooses its windows per CTA)
-    const bool fast = n > 0 && !h->spec.deterministic && fast_eligible(in, S.acc, geom.ndim);
-    const bool window_in_prep = !geom.bounds_auto && !h->spec.deterministic && !fast;
+    bool fast = n > 0 && !h->spec.deterministic && !part && fast_eligible(in, S.acc, geom.ndim);
+    const bool window_in_prep = !geom.bounds_auto && !h->spec.deterministic && !fast && !part;
     if ((e = launch_init(geom, in, S.acc, h->wcap, window_in_prep, s)) != cudaSuccess)
         return cuda_error(e, "init kernel");
     S.launches++;
@@ -552,6 +643,32 @@ int bin_execute(bin_handle_t *h, bin_array_t *const *axes, int32_t naxes, bin_ar
         if (h->comm) {
             ncclResult_t r = ncclAllReduce(S.acc.bounds, S.acc.bounds, 2 * geom.ndim, ncclUint64, ncclMin, h->comm, s);
             if (r != ncclSuccess) return nccl_error(r, "ncclAllReduce(bounds)");
+        }
+    }
+    // ---- route probe (auto): first execute synchronously, then every ROUTE_REPROBE
+    // executes in the background (read back at a later execute, never waited for)
+    if (part_ok && h->spec.route == BIN_ROUTE_AUTO && !h->probe_inflight &&
+        (h->route == 0 || ++h->since_probe >= ROUTE_REPROBE)) {
+        if (!h->probe_d) {
+            DB_CUDA(cudaMalloc(&h->probe_d, 64));
+            count_alloc(64);
+            DB_CUDA(cudaHostAlloc((void **)&h->probe_h, 64, cudaHostAllocPortable));
+            count_alloc(64);
+            DB_CUDA(cudaEventCreateWithFlags(&h->probe_ev, cudaEventDisableTiming));
+        }
+        if ((e = launch_probe(geom, in, S.acc, h->wcap, h->probe_d, s)) != cudaSuccess)
+            return cuda_error(e, "route probe kernel");
+        S.launches++;
+        DB_CUDA(cudaMemcpyAsync(h->probe_h, h->probe_d, 8 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        DB_CUDA(cudaEventRecord(h->probe_ev, s));
+        h->probe_inflight = true;
+        h->since_probe = 0;
+        if (h->route == 0) {
+            DB_CUDA(cudaEventSynchronize(h->probe_ev));
+            h->route = probe_route(h->probe_h);
+            h->probe_inflight = false;
+            part = h->route == BIN_ROUTE_PARTITION;
+            fast = fast && !part;
         }
     }
     if ((rc = rec(EV_BOUNDS1))) return rc;
@@ -567,20 +684,29 @@ int bin_execute(bin_handle_t *h, bin_array_t *const *axes, int32_t naxes, bin_ar
         variant = 3;
     } else {
         // ---- hot-window choice, then a4 + a5
-        if (!window_in_prep && !fast) {
+        if (!window_in_prep && !fast && !part && n > 0) {
             if ((e = launch_window(geom, in, S.acc, h->wcap, s)) != cudaSuccess) return cuda_error(e, "window kernel");
             S.launches += 1;
         }
         if ((rc = rec(EV_WINDOW1))) return rc;
         if (n / h->lc.sms >= (int64_t)0xffffffffLL)
             return set_error(BIN_EINVAL, "%lld rows per call exceed the per-CTA u32 window counters", (long long)n);
-        if (n > 0) {
-            e = fast ? launch_bin_fast(geom, in, S.acc, h->lc, h->smem_bytes, h->wcap, s)
-                     : launch_bin_general(geom, in, S.acc, h->lc, h->smem_bytes, s);
-            if (e != cudaSuccess) return cuda_error(e, "bin kernel");
-            S.launches++, S.bin_launches++;
+        if (part) {
+            if ((rc = ensure_part_scratch(h, n, pa))) return rc;
+            int pl = 0;
+            if ((e = launch_partition(geom, in, S.acc, pa, s, &pl)) != cudaSuccess)
+                return cuda_error(e, "partition route kernels");
+            S.launches += pl, S.bin_launches += pl;
+            variant = 4;
+        } else {
+            if (n > 0) {
+                e = fast ? launch_bin_fast(geom, in, S.acc, h->lc, h->smem_bytes, h->wcap, s)
+                         : launch_bin_general(geom, in, S.acc, h->lc, h->smem_bytes, s);
+                if (e != cudaSuccess) return cuda_error(e, "bin kernel");
+                S.launches++, S.bin_launches++;
+            }
+            variant = ((uint64_t)h->wcap >= h->nbins ? 2 : 1) | (fast ? 16 : 0);
         }
-        variant = ((uint64_t)h->wcap >= h->nbins ? 2 : 1) | (fast ? 16 : 0);
     }
     if ((rc = rec(EV_BIN1))) return rc;
     // ---- a6 + a7 fused over NVLink peer memory (one kernel), or NCCL + finalize
@@ -781,6 +907,22 @@ int bin_finalize(bin_handle_t *h) {
         for (auto &e : h->producer_ev)
             if (e) cudaEventDestroy(e), e = nullptr;
         free_det_scratch(h->det);
+        if (h->part_base) {
+            cudaFree(h->part_base);
+            count_free((int64_t)h->part_bytes);
+            h->part_base = nullptr;
+        }
+        if (h->probe_d) {
+            cudaFree(h->probe_d);
+            count_free(64);
+            h->probe_d = nullptr;
+        }
+        if (h->probe_h) {
+            cudaFreeHost(h->probe_h);
+            count_free(64);
+            h->probe_h = nullptr;
+        }
+        if (h->probe_ev) cudaEventDestroy(h->probe_ev), h->probe_ev = nullptr;
         if (h->gather) {
             cudaFree(h->gather);
             count_free((int64_t)h->gather_bytes);

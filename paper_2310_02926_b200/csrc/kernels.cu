@@ -37,14 +37,19 @@ constexpr int WIN_SAMPLES = 16384;
 constexpr int PREP_THREADS = 512;
 constexpr int WIN_BATCH = 8;  // sample rows per thread in flight
 
-// Best box from the coarse histogram in shared memory -> acc.window.
-__device__ void window_pick(const Geom &g, const DGeom &G, const WinPlan &P, const Accum &acc, unsigned *hist,
+// Best box from the coarse histogram in shared memory -> win[0..5] (origin,
+// extent); win[6], win[7] = sampled rows in the box / inside the grid.
+__device__ void window_pick(const Geom &g, const DGeom &G, const WinPlan &P, int32_t *win, unsigned *hist,
                             unsigned long long *best) {
-    __shared__ int origin[4];
+    __shared__ int origin[6];
     if (P.skip || P.full) {
         if (threadIdx.x < 3) {
-            acc.window[threadIdx.x] = 0;
-            acc.window[3 + threadIdx.x] = P.skip ? 0 : G.res[threadIdx.x];
+            win[threadIdx.x] = 0;
+            win[3 + threadIdx.x] = P.skip ? 0 : G.res[threadIdx.x];
+        }
+        if (threadIdx.x == 0) {
+            win[6] = P.full ? 1 : 0;
+            win[7] = 1;
         }
         return;
     }
@@ -54,13 +59,19 @@ __device__ void window_pick(const Geom &g, const DGeom &G, const WinPlan &P, con
     default: pick_box<3>(P, G.res[0], G.res[1], G.res[2], hist, best, origin); break;
     }
     if (threadIdx.x < 3) {
-        acc.window[threadIdx.x] = origin[threadIdx.x];
-        acc.window[3 + threadIdx.x] = P.e[threadIdx.x];
+        win[threadIdx.x] = origin[threadIdx.x];
+        win[3 + threadIdx.x] = P.e[threadIdx.x];
+    }
+    if (threadIdx.x == 0) {
+        win[6] = origin[4];
+        win[7] = origin[5];
     }
 }
 
-// One CTA: sample, coarse histogram in shared memory, pick.
-__device__ __forceinline__ void window_choose(const Geom &g, const Inputs &in, const Accum &acc, int wcap) {
+// One CTA: sample, coarse histogram in shared memory, pick -> win[0..7];
+// with `exps` also the sampled exponent maxima -> acc.fxexp.
+__device__ __forceinline__ void window_choose(const Geom &g, const Inputs &in, const Accum &acc, int wcap, int32_t *win,
+                                              bool exps) {
     __shared__ unsigned hist[WIN_CELLS];
     __shared__ unsigned long long best[PREP_THREADS / 32];
     const DGeom G = load_geom(g, acc.bounds);
@@ -72,7 +83,7 @@ __device__ __forceinline__ void window_choose(const Geom &g, const Inputs &in, c
     const int64_t S = in.n < WIN_SAMPLES ? in.n : WIN_SAMPLES;
     const int64_t stride = work ? in.n / S : 1;
     // largest exponent of each summed attribute over the sample
-    for (int a = 0; work && a < in.nattr; ++a) {
+    for (int a = 0; exps && work && a < in.nattr; ++a) {
         if (!((acc.sum_mask >> a) & 1u)) continue;
         unsigned emax = 0u;
         for (int64_t j0 = threadIdx.x; j0 < S; j0 += (int64_t)blockDim.x * WIN_BATCH) {
@@ -119,12 +130,23 @@ __device__ __forceinline__ void window_choose(const Geom &g, const Inputs &in, c
         }
     }
     __syncthreads();
-    window_pick(g, G, P, acc, hist, best);
+    window_pick(g, G, P, win, hist, best);
+}
+
+// Route probe (handle.cpp): the window a CTA would get for wcap bins, and how
+// many of 16,384 sampled rows it would hold -> out[0..7] (device memory).
+__global__ void __launch_bounds__(PREP_THREADS) k_probe(Geom g, Inputs in, Accum acc, int wcap, int32_t *out) {
+    window_choose(g, in, acc, wcap, out, false);
+}
+
+cudaError_t launch_probe(const Geom &g, const Inputs &in, const Accum &acc, int wcap, int32_t *out, cudaStream_t s) {
+    k_probe<<<1, PREP_THREADS, 0, s>>>(g, in, acc, wcap, out);
+    return cudaGetLastError();
 }
 
 __global__ void __launch_bounds__(PREP_THREADS) k_prep(Geom g, Inputs in, Accum acc, int wcap, int choose) {
     if (choose && blockIdx.x == 0) {  // manual bounds: the window needs no other input
-        window_choose(g, in, acc, wcap);
+        window_choose(g, in, acc, wcap, acc.window, true);
         return;
     }
     const int zb = choose ? (int)blockIdx.x - 1 : (int)blockIdx.x, nzb = choose ? gridDim.x - 1 : gridDim.x;
@@ -139,7 +161,7 @@ __global__ void __launch_bounds__(PREP_THREADS) k_prep(Geom g, Inputs in, Accum 
 }
 
 __global__ void __launch_bounds__(PREP_THREADS) k_window(Geom g, Inputs in, Accum acc, int wcap) {
-    window_choose(g, in, acc, wcap);
+    window_choose(g, in, acc, wcap, acc.window, true);
 }
 
 cudaError_t launch_init(const Geom &g, const Inputs &in, const Accum &acc, int wcap, bool choose_window,

@@ -19,7 +19,7 @@ def bits(x):
 
 
 def run_gpu(db, axes, attrs, res, lo=None, hi=None, ops=ALL_OPS, bounds_auto=False, deterministic=False,
-            placement=None, offset=0, host_inputs=False, device=0, return_handle=False):
+            placement=None, offset=0, host_inputs=False, device=0, return_handle=False, route="auto"):
     import torch
     dev = torch.device(f"cuda:{device}")
     cols = list(axes) + list(attrs)
@@ -38,7 +38,7 @@ def run_gpu(db, axes, attrs, res, lo=None, hi=None, ops=ALL_OPS, bounds_auto=Fal
         handles.append(db.wrap_tensor(t))
     torch.cuda.synchronize(dev)
     spec = db.make_spec(res, lo, hi, nattr=len(attrs), ops=ops, bounds_auto=bounds_auto,
-                        deterministic=deterministic)
+                        deterministic=deterministic, route=route)
     pl = placement if placement is not None else db.make_placement(device_id=device)
     h = db.bin_init(spec, pl)
     db.bin_profile_enable(h, True)

@@ -142,8 +142,9 @@ def test_ragged_sizes_and_alignment(db, n, offset):
     rng = np.random.default_rng(n)
     axes = [rng.uniform(-1.1, 1.1, n), rng.uniform(-1.1, 1.1, n)]
     attrs = [rng.uniform(0.5, 1.5, n)]
-    for res in ([16, 16], [512, 512]):          # full-grid smem variant and the window variant
-        both(db, axes, attrs, res, [-1, -1], [1, 1], offset=offset, det_too=(n < 5000))
+    both(db, axes, attrs, [16, 16], [-1, -1], [1, 1], offset=offset, det_too=(n < 5000))   # full-grid window
+    for route in ("window", "partition"):       # 512^2: hot window + L2, and the partition route
+        both(db, axes, attrs, [512, 512], [-1, -1], [1, 1], offset=offset, det_too=False, route=route)
 
 
 def test_mixed_alignment_falls_back_to_scalar(db):
@@ -173,6 +174,7 @@ def test_3d_global_path_and_window(db):
     axes = [rng.uniform(-1, 1, n) for _ in range(3)]
     attrs = [rng.uniform(0.5, 1.5, n)]
     both(db, axes, attrs, [64, 64, 64], [-1] * 3, [1] * 3, det_too=True)
+    both(db, axes, attrs, [64, 64, 64], [-1] * 3, [1] * 3, det_too=False, route="window")
     axes = [rng.standard_normal(n) * 0.1 for _ in range(3)]       # clustered: window catches most rows
     out, _ = both(db, axes, attrs, [128, 128, 128], [-1] * 3, [1] * 3, det_too=False)
     assert out["profile"].variant & 15 == 1
