@@ -433,6 +433,15 @@ int bin_init(const bin_spec_t *spec, const bin_placement_t *place, const bin_com
         return fail(cuda_error(ce, "cudaStreamCreate"));
     if ((ce = cudaStreamCreateWithFlags(&h->copy, cudaStreamNonBlocking)) != cudaSuccess)
         return fail(cuda_error(ce, "cudaStreamCreate"));
+    if (!h->spec.deterministic && h->spec.route == BIN_ROUTE_AUTO) {  // route probe buffers (executes allocate nothing)
+        if ((ce = cudaMalloc(&h->probe_d, 64)) != cudaSuccess) return fail(cuda_error(ce, "cudaMalloc(probe)"));
+        count_alloc(64);
+        if ((ce = cudaHostAlloc((void **)&h->probe_h, 64, cudaHostAllocPortable)) != cudaSuccess)
+            return fail(cuda_error(ce, "cudaHostAlloc(probe)"));
+        count_alloc(64);
+        if ((ce = cudaEventCreateWithFlags(&h->probe_ev, cudaEventDisableTiming)) != cudaSuccess)
+            return fail(cuda_error(ce, "cudaEventCreate(probe)"));
+    }
     // direct NVLink access to every other GPU this one can reach (peer copies and
     // the peer combine); without it cudaMemcpyPeerAsync stages through the host
     for (int d = 0; d < n_a; ++d) {
@@ -649,13 +658,6 @@ int bin_execute(bin_handle_t *h, bin_array_t *const *axes, int32_t naxes, bin_ar
     // executes in the background (read back at a later execute, never waited for)
     if (part_ok && h->spec.route == BIN_ROUTE_AUTO && !h->probe_inflight &&
         (h->route == 0 || ++h->since_probe >= ROUTE_REPROBE)) {
-        if (!h->probe_d) {
-            DB_CUDA(cudaMalloc(&h->probe_d, 64));
-            count_alloc(64);
-            DB_CUDA(cudaHostAlloc((void **)&h->probe_h, 64, cudaHostAllocPortable));
-            count_alloc(64);
-            DB_CUDA(cudaEventCreateWithFlags(&h->probe_ev, cudaEventDisableTiming));
-        }
         if ((e = launch_probe(geom, in, S.acc, h->wcap, h->probe_d, s)) != cudaSuccess)
             return cuda_error(e, "route probe kernel");
         S.launches++;

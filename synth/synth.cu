@@ -14,7 +14,53 @@ __global__ void syn_fill_kernel(int dist, int central, uint64_t seed, int column
         out[i] = syn_value(dist, central, seed, column, start + (uint64_t)i);
 }
 
+// A Newton++-shaped O(N) producer for the placement study (BASELINE.json
+// configs[4]): one second-order, time-reversible kick-drift-kick leapfrog step
+// of every body in the softened field of the massive body at the origin
+// (G = 1).  It stands in for the paper's O(N^2) direct-sum solver (out of
+// scope); it reads 7 and writes 6 columns per body (104 B), like a solver
+// step's streaming cost.  Not part of the binning method.
+__global__ void syn_kdk_kernel(double *x, double *y, double *z, double *vx, double *vy, double *vz, int64_t n,
+                               double central_mass, double eps2, double dt) {
+    const double hdt = 0.5 * dt;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        if (i == 0) continue;  // the massive body stays at the origin
+        double px = x[i], py = y[i], pz = z[i], ux = vx[i], uy = vy[i], uz = vz[i];
+        double r2 = SYN_ADD(SYN_ADD(SYN_ADD(SYN_MUL(px, px), SYN_MUL(py, py)), SYN_MUL(pz, pz)), eps2);
+        double inv = SYN_DIV(central_mass, SYN_MUL(r2, SYN_SQRT(r2)));
+        ux = SYN_SUB(ux, SYN_MUL(hdt, SYN_MUL(px, inv)));
+        uy = SYN_SUB(uy, SYN_MUL(hdt, SYN_MUL(py, inv)));
+        uz = SYN_SUB(uz, SYN_MUL(hdt, SYN_MUL(pz, inv)));
+        px = SYN_ADD(px, SYN_MUL(dt, ux));
+        py = SYN_ADD(py, SYN_MUL(dt, uy));
+        pz = SYN_ADD(pz, SYN_MUL(dt, uz));
+        r2 = SYN_ADD(SYN_ADD(SYN_ADD(SYN_MUL(px, px), SYN_MUL(py, py)), SYN_MUL(pz, pz)), eps2);
+        inv = SYN_DIV(central_mass, SYN_MUL(r2, SYN_SQRT(r2)));
+        vx[i] = SYN_SUB(ux, SYN_MUL(hdt, SYN_MUL(px, inv)));
+        vy[i] = SYN_SUB(uy, SYN_MUL(hdt, SYN_MUL(py, inv)));
+        vz[i] = SYN_SUB(uz, SYN_MUL(hdt, SYN_MUL(pz, inv)));
+        x[i] = px;
+        y[i] = py;
+        z[i] = pz;
+    }
+}
+
 extern "C" {
+
+// One KDK step of n bodies (device columns), enqueued on `stream`.
+int synth_kdk_step(double *x, double *y, double *z, double *vx, double *vy, double *vz, int64_t n,
+                   double central_mass, double eps2, double dt, void *stream) {
+    if (n <= 0) return 0;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > (int64_t)sms * 8) blocks = (int64_t)sms * 8;
+    syn_kdk_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(x, y, z, vx, vy, vz, n, central_mass, eps2, dt);
+    return (int)cudaGetLastError();
+}
+
 
 // Fill out[0..n) with column `column` of rows start..start+n-1 on the host.
 int synth_fill_host(int dist, int central, uint64_t seed, int column, uint64_t start, int64_t n,

@@ -176,8 +176,9 @@ def test_3d_global_path_and_window(db):
     both(db, axes, attrs, [64, 64, 64], [-1] * 3, [1] * 3, det_too=True)
     both(db, axes, attrs, [64, 64, 64], [-1] * 3, [1] * 3, det_too=False, route="window")
     axes = [rng.standard_normal(n) * 0.1 for _ in range(3)]       # clustered: window catches most rows
-    out, _ = both(db, axes, attrs, [128, 128, 128], [-1] * 3, [1] * 3, det_too=False)
+    out, _ = both(db, axes, attrs, [128, 128, 128], [-1] * 3, [1] * 3, det_too=False, route="window")
     assert out["profile"].variant & 15 == 1
+    both(db, axes, attrs, [128, 128, 128], [-1] * 3, [1] * 3, det_too=False)   # auto (either route)
 
 
 def test_zero_rows_and_degenerate_bounds(db):
