@@ -56,14 +56,16 @@ def main():
         torch.cuda.synchronize(dev)
         hs = [db.wrap_tensor(t) for t in cols]
         D = len(w.axes)
-        for det in (False, True):
+        for det, route in ((False, "auto"), (False, "window"), (False, "partition"), (True, "auto")):
             obj = [db.bin_nccl_unique_id() if rank == 0 else None]
             dist.broadcast_object_list(obj, src=0)
             spec = db.make_spec(res, None if auto else w.lo, None if auto else w.hi, nattr=len(w.attrs),
-                                ops=w.ops, bounds_auto=auto, deterministic=det)
+                                ops=w.ops, bounds_auto=auto, deterministic=det, route=route)
             h = db.bin_init(spec, db.make_placement(), rank=rank, nranks=world, nccl_id=obj[0])
+            db.bin_profile_enable(h, True)
             t = db.bin_execute(h, hs[:D], hs[D:])
             out = db.result_to_numpy(h, t, spec)
+            variant = db.bin_profile_read(h).variant
             db.bin_finalize(h)
             if rank == 0:
                 import oracle
@@ -79,7 +81,8 @@ def main():
                 except AssertionError as e:  # noqa: PERF203
                     status = "FAIL: " + str(e)[:300]
                     ok = False
-                print(json.dumps({"case": name, "deterministic": det, "world": world, "rows": n,
+                print(json.dumps({"case": name, "deterministic": det, "route": route, "variant": variant,
+                                  "world": world, "rows": n,
                                   "res": list(res), "status": status, "n_in": out["n_in"],
                                   "n_out": out["n_out"]}), flush=True)
             dist.barrier()

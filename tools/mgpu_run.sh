@@ -6,17 +6,11 @@ timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --mas
 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29512 bench.py --gpus $N --steps 100 --warmup 5 --no-cpu-baseline > gpurun_out/bench_n$N.json 2> gpurun_out/bench_n$N.err; echo bench=$?
 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29513 bench.py --gpus $N --steps 100 --warmup 5 --no-cpu-baseline --no-e2e --scaling weak > gpurun_out/bench_n${N}_weak.json 2>> gpurun_out/bench_n$N.err; echo bench_weak=$?
 cat gpurun_out/mgpu_check_$N.log | grep -E "case|Error|FAIL" | head -20
-python -c "
-import json
-for f in ['gpurun_out/bench_n$N.json','gpurun_out/bench_n${N}_weak.json']:
-    try:
-        d=json.loads([l for l in open(f) if l.startswith("{")][-1]); print(f, round(d['value']/1e9,1), 'G/s', d['ms_per_step'], d['phases_ms_per_step'])
-    except Exception as e: print(f, 'ERR', e)
-"
+if [ "${C4:-0}" = "1" ]; then
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29515 bench.py --gpus $N --workload c4 --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_n${N}_c4.json 2>> gpurun_out/bench_n$N.err; echo bench_c4=$?
+fi
+python tools/bench_lines.py gpurun_out/bench_n$N.json gpurun_out/bench_n${N}_weak.json gpurun_out/bench_n${N}_c4.json
 if [ "${AB_NCCL:-0}" = "1" ]; then
 DATABIN_COMBINE=nccl timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29514 bench.py --gpus $N --steps 100 --warmup 5 --no-cpu-baseline --no-e2e > gpurun_out/bench_n${N}_nccl.json 2>> gpurun_out/bench_n$N.err; echo bench_nccl=$?
-python -c "
-import json
-d=json.loads([l for l in open('gpurun_out/bench_n${N}_nccl.json') if l.startswith('{')][-1]); print('nccl combine', round(d['value']/1e9,1), 'G/s', d['ms_per_step'], d['phases_ms_per_step'])
-"
+python tools/bench_lines.py gpurun_out/bench_n${N}_nccl.json
 fi
