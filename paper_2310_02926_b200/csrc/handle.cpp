@@ -26,6 +26,7 @@ struct Slot {
     Meta *meta_h = nullptr, *meta_d = nullptr;
     cudaEvent_t done = nullptr, released = nullptr;
     cudaEvent_t ev[EV_N] = {};
+    bool recd[EV_N] = {};  // which events this execute recorded (profiling)
     bool prof_pending = false;
     bool meta_valid = false;
     uint64_t ticket = 0;
@@ -504,6 +505,25 @@ static int stage_buffer(bin_handle *h, int sl, int col, size_t bytes, void **p) 
     return BIN_OK;
 }
 
+// k_probe + D2H of its 8 ints; `wait`: block until the route is known (first
+// execute), else leave it in flight (read back by a later execute).
+static int run_probe(bin_handle *h, const Geom &geom, const Inputs &in, Slot &S, cudaStream_t s, bool wait) {
+    cudaError_t e;
+    if ((e = launch_probe(geom, in, S.acc, h->wcap, h->probe_d, s)) != cudaSuccess)
+        return cuda_error(e, "route probe kernel");
+    S.launches++;
+    DB_CUDA(cudaMemcpyAsync(h->probe_h, h->probe_d, 8 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    DB_CUDA(cudaEventRecord(h->probe_ev, s));
+    h->probe_inflight = true;
+    h->since_probe = 0;
+    if (wait) {
+        DB_CUDA(cudaEventSynchronize(h->probe_ev));
+        h->route = probe_route(h->probe_h);
+        h->probe_inflight = false;
+    }
+    return BIN_OK;
+}
+
 int bin_execute(bin_handle_t *h, bin_array_t *const *axes, int32_t naxes, bin_array_t *const *attrs,
                 int32_t nattr, uint64_t *ticket) {
     if (!h || h->finalized) return set_error(BIN_ESTATE, "bin_execute: handle is NULL or finalized");
@@ -545,7 +565,11 @@ int bin_execute(bin_handle_t *h, bin_array_t *const *axes, int32_t naxes, bin_ar
     S.launches = 0;
     S.bin_launches = 0;
     h->last = s;
-    if (h->prof) DB_CUDA(cudaEventRecord(S.ev[EV_STAGE], s));
+    for (bool &r : S.recd) r = false;
+    if (h->prof) {
+        DB_CUDA(cudaEventRecord(S.ev[EV_STAGE], s));
+        S.recd[EV_STAGE] = true;
+    }
 
     // ---- a1: resolve input views on the analysis device.  Columns already on
     // it are read in place (zero copy); the others -- host memory, another GPU
@@ -615,12 +639,17 @@ int bin_execute(bin_handle_t *h, bin_array_t *const *axes, int32_t naxes, bin_ar
         geom.hi[d] = d < geom.ndim ? h->spec.hi[d] : 1.0;
     }
     cudaError_t e;
-    auto rec = [&](int k) -> int {
-        if (h->prof) DB_CUDA(cudaEventRecord(S.ev[k], s));
+    // profiling: an event only after a phase that enqueued work (an event costs
+    // ~2-3 us of stream time; empty phases get none and read as 0)
+    auto rec = [&](int k, bool work) -> int {
+        if (h->prof && work) {
+            DB_CUDA(cudaEventRecord(S.ev[k], s));
+            S.recd[k] = true;
+        }
         return BIN_OK;
     };
     int rc;
-    if ((rc = rec(EV_INIT0))) return rc;
+    if ((rc = rec(EV_INIT0, staged_any))) return rc;
     // ---- route: partition (bin_part.cu) or window; auto follows the last probe
     PartArgs pa{};
     const bool part_ok = n > 0 && !h->spec.deterministic && h->spec.route != BIN_ROUTE_WINDOW &&
@@ -636,6 +665,13 @@ int bin_execute(bin_handle_t *h, bin_array_t *const *axes, int32_t naxes, bin_ar
             return cuda_error(q, "route probe");
         }
     }
+    // first execute with manual bounds: the synchronous probe runs before the
+    // init so that the route (and the one-launch step) is known from the start
+    bool probed = false;
+    if (part_ok && h->spec.route == BIN_ROUTE_AUTO && h->route == 0 && !geom.bounds_auto) {
+        if ((rc = run_probe(h, geom, in, S, s, true))) return rc;
+        probed = true;
+    }
     bool part = part_ok && (h->spec.route == BIN_ROUTE_PARTITION || h->route == BIN_ROUTE_PARTITION);
     // ---- a3: accumulator identities (+ the window choice when the bounds are manual
     // and the general kernel will run; k_bin_fast chooses its windows per CTA)
@@ -644,7 +680,7 @@ int bin_execute(bin_handle_t *h, bin_array_t *const *axes, int32_t naxes, bin_ar
     if ((e = launch_init(geom, in, S.acc, h->wcap, window_in_prep, s)) != cudaSuccess)
         return cuda_error(e, "init kernel");
     S.launches++;
-    if ((rc = rec(EV_INIT1))) return rc;
+    if ((rc = rec(EV_INIT1, true))) return rc;
     // ---- a2: automatic bounds (+ cross-rank Min, reading R3)
     if (geom.bounds_auto) {
         if ((e = launch_bounds(geom, in, S.acc, h->lc, s)) != cudaSuccess) return cuda_error(e, "bounds kernel");
@@ -656,27 +692,20 @@ int bin_execute(bin_handle_t *h, bin_array_t *const *axes, int32_t naxes, bin_ar
     }
     // ---- route probe (auto): first execute synchronously, then every ROUTE_REPROBE
     // executes in the background (read back at a later execute, never waited for)
-    if (part_ok && h->spec.route == BIN_ROUTE_AUTO && !h->probe_inflight &&
+    if ((rc = rec(EV_BOUNDS1, geom.bounds_auto))) return rc;
+    if (part_ok && h->spec.route == BIN_ROUTE_AUTO && !h->probe_inflight && !probed &&
         (h->route == 0 || ++h->since_probe >= ROUTE_REPROBE)) {
-        if ((e = launch_probe(geom, in, S.acc, h->wcap, h->probe_d, s)) != cudaSuccess)
-            return cuda_error(e, "route probe kernel");
-        S.launches++;
-        DB_CUDA(cudaMemcpyAsync(h->probe_h, h->probe_d, 8 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-        DB_CUDA(cudaEventRecord(h->probe_ev, s));
-        h->probe_inflight = true;
-        h->since_probe = 0;
-        if (h->route == 0) {
-            DB_CUDA(cudaEventSynchronize(h->probe_ev));
-            h->route = probe_route(h->probe_h);
-            h->probe_inflight = false;
+        const bool first = h->route == 0;
+        if ((rc = run_probe(h, geom, in, S, s, first))) return rc;
+        probed = true;
+        if (first) {
             part = h->route == BIN_ROUTE_PARTITION;
             fast = fast && !part;
         }
     }
-    if ((rc = rec(EV_BOUNDS1))) return rc;
     int variant;
     if (h->spec.deterministic) {
-        if ((rc = rec(EV_WINDOW1))) return rc;
+        if ((rc = rec(EV_WINDOW1, probed))) return rc;
         int launches = 0;
         if ((rc = ensure_det_scratch(h->det, n, h->nbins, h->device, h->lc.sms))) return rc;
         if ((e = launch_deterministic(geom, in, S.acc, h->det, h->lc, s, &launches)) != cudaSuccess)
@@ -686,11 +715,12 @@ int bin_execute(bin_handle_t *h, bin_array_t *const *axes, int32_t naxes, bin_ar
         variant = 3;
     } else {
         // ---- hot-window choice, then a4 + a5
-        if (!window_in_prep && !fast && !part && n > 0) {
+        const bool win_kernel = !window_in_prep && !fast && !part && n > 0;
+        if (win_kernel) {
             if ((e = launch_window(geom, in, S.acc, h->wcap, s)) != cudaSuccess) return cuda_error(e, "window kernel");
             S.launches += 1;
         }
-        if ((rc = rec(EV_WINDOW1))) return rc;
+        if ((rc = rec(EV_WINDOW1, win_kernel || probed))) return rc;
         if (n / h->lc.sms >= (int64_t)0xffffffffLL)
             return set_error(BIN_EINVAL, "%lld rows per call exceed the per-CTA u32 window counters", (long long)n);
         if (part) {
@@ -701,25 +731,24 @@ int bin_execute(bin_handle_t *h, bin_array_t *const *axes, int32_t naxes, bin_ar
             S.launches += pl, S.bin_launches += pl;
             variant = 4;
         } else {
+            variant = ((uint64_t)h->wcap >= h->nbins ? 2 : 1) | (fast ? 16 : 0);
             if (n > 0) {
                 e = fast ? launch_bin_fast(geom, in, S.acc, h->lc, h->smem_bytes, h->wcap, s)
                          : launch_bin_general(geom, in, S.acc, h->lc, h->smem_bytes, s);
                 if (e != cudaSuccess) return cuda_error(e, "bin kernel");
                 S.launches++, S.bin_launches++;
             }
-            variant = ((uint64_t)h->wcap >= h->nbins ? 2 : 1) | (fast ? 16 : 0);
         }
     }
-    if ((rc = rec(EV_BIN1))) return rc;
+    if ((rc = rec(EV_BIN1, n > 0))) return rc;
     // ---- a6 + a7 fused over NVLink peer memory (one kernel), or NCCL + finalize
     if (h->peer) {
-        if ((rc = rec(EV_COMBINE1))) return rc;
         if ((e = launch_combine_peer(geom, S.peers, h->rank, h->nranks, t, S.meta_d, variant | 32,
                                      h->spec.deterministic, h->lc.sms, s)) != cudaSuccess)
             return cuda_error(e, "peer combine kernel");
         S.launches++;
         S.variant = variant | 32;
-        if ((rc = rec(EV_FINAL1))) return rc;
+        if ((rc = rec(EV_FINAL1, true))) return rc;
     } else {
     // ---- a6: cross-rank combine over NVLink (one NCCL group)
     if (h->comm) {
@@ -741,12 +770,12 @@ int bin_execute(bin_handle_t *h, bin_array_t *const *axes, int32_t naxes, bin_ar
             S.launches++;
         }
     }
-    if ((rc = rec(EV_COMBINE1))) return rc;
+    if ((rc = rec(EV_COMBINE1, h->comm != nullptr))) return rc;
     // ---- a7: finalize
     if ((e = launch_finalize(geom, S.acc, S.meta_d, n, variant, s)) != cudaSuccess) return cuda_error(e, "finalize kernel");
     S.launches++;
     S.variant = variant;
-    if ((rc = rec(EV_FINAL1))) return rc;
+    if ((rc = rec(EV_FINAL1, true))) return rc;
     }
     DB_CUDA(cudaEventRecord(S.done, s));
     if (!staged_any) DB_CUDA(cudaEventRecord(S.released, s));
@@ -789,7 +818,11 @@ static void accumulate_profile(bin_handle *h, Slot &S) {
     S.prof_pending = false;
     fetch_meta(h, S);
     float ms[EV_N] = {};
-    for (int k = 1; k < EV_N; ++k) cudaEventElapsedTime(&ms[k], S.ev[k - 1], S.ev[k]);
+    for (int k = 1, last = EV_STAGE; k < EV_N; ++k)
+        if (S.recd[k]) {  // a phase's time runs from the previous recorded event
+            cudaEventElapsedTime(&ms[k], S.ev[last], S.ev[k]);
+            last = k;
+        }
     cudaGetLastError();
     bin_profile_t &p = h->pacc;
     p.ms_stage += ms[EV_INIT0];

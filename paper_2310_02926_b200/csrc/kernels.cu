@@ -22,6 +22,7 @@
 
 #include "db_internal.h"
 #include "dev_common.cuh"
+#include "tail.cuh"
 
 namespace db {
 // ---------------------------------------------------------------- init [a3] + window
@@ -235,53 +236,8 @@ cudaError_t launch_bounds(const Geom &g, const Inputs &in, const Accum &acc, con
 }
 
 // ---------------------------------------------------------------- finalize [a7]
-__global__ void k_finalize(Geom g, Accum acc, Meta *meta, int variant) {
-    DGeom G = load_geom(g, acc.bounds);
-    const uint64_t nb = acc.nbins;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (G.ok && acc.nsum <= 1 && acc.nmm <= 1) {
-        // common case: issue the bin's loads together (one latency, not three)
-        for (int64_t b = t0; b < (int64_t)nb; b += stride) {
-            const unsigned long long cnt = acc.count[b];
-            const double sm = acc.nsum ? acc.sum[b] : 0.0;
-            const ulonglong2 m = acc.nmm ? ((const ulonglong2 *)acc.mm)[b] : make_ulonglong2(0ull, 0ull);
-            if (acc.nsum) acc.oavg[b] = cnt ? __ddiv_rn(sm, (double)cnt) : __longlong_as_double(0x7ff8000000000000ll);
-            if (acc.nmm) {
-                acc.omin[b] = cnt ? dec_total(m.x) : __longlong_as_double(0x7ff0000000000000ll);
-                acc.omax[b] = cnt ? dec_total(~m.y) : __longlong_as_double((long long)0xfff0000000000000ull);
-            }
-        }
-    } else if (G.ok) {
-        for (int64_t b = t0; b < (int64_t)nb; b += stride) {
-            const unsigned long long cnt = acc.count[b];
-            const double dc = (double)cnt;
-            for (int s = 0; s < acc.nsum; ++s) {
-                const double sm = acc.sum[(uint64_t)s * nb + b];
-                acc.oavg[(uint64_t)s * nb + b] = cnt ? __ddiv_rn(sm, dc) : __longlong_as_double(0x7ff8000000000000ll);
-            }
-            for (int s = 0; s < acc.nmm; ++s) {
-                const ulonglong2 m = ((const ulonglong2 *)acc.mm)[(uint64_t)s * nb + b];
-                acc.omin[(uint64_t)s * nb + b] = cnt ? dec_total(m.x) : __longlong_as_double(0x7ff0000000000000ll);
-                acc.omax[(uint64_t)s * nb + b] = cnt ? dec_total(~m.y) : __longlong_as_double((long long)0xfff0000000000000ull);
-            }
-        }
-    }
-    if (t0 == 0) {
-        meta->status = G.ok ? 0 : BIN_EDEGENERATE;
-        meta->variant = variant;
-        meta->n_in = acc.count[nb];
-        meta->n_out = acc.count[nb + 1];
-        for (int d = 0; d < 3; ++d) {
-            meta->lo[d] = G.lo[d];
-            meta->hi[d] = G.hi[d];
-            meta->window[d] = acc.window[d];
-            meta->window[3 + d] = acc.window[3 + d];
-        }
-        meta->done = 1;  // device memory; the host copies it on demand (bin_wait)
-    }
-    if (t0 < BIN_MAX_ATTR) acc.fxexp[t0] = 0u;  // for the next execute's sample on this slot
-}
+// (body in tail.cuh)
+__global__ void k_finalize(Geom g, Accum acc, Meta *meta, int variant) { finalize_body(g, acc, meta, variant); }
 
 cudaError_t launch_finalize(const Geom &g, const Accum &acc, Meta *meta_dev, int64_t n_rows_local, int variant,
                             cudaStream_t s) {
