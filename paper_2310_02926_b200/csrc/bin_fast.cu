@@ -240,7 +240,7 @@ __device__ __forceinline__ void fast_choose_window(const DGeom G, const WinPlan 
 
 template <int D, int A, int SM, int MM>
 __global__ void __launch_bounds__(FAST_THREADS, 1)
-    k_bin_fast(Geom g, Inputs in, Accum acc, uint32_t npairs, int head, int wcap) {
+    k_bin_fast(Geom g, Inputs in, Accum acc, uint32_t npairs, int head, int wcap, int32_t *wcache, int reuse) {
     constexpr bool HS = A == 1 && SM == 1, HM = A == 1 && MM == 1;
     __shared__ unsigned long long s_best[FAST_THREADS / 32];
     __shared__ int s_origin[6];
@@ -262,8 +262,18 @@ __global__ void __launch_bounds__(FAST_THREADS, 1)
         if (!G.ok) return;  // degenerate auto bounds: finalize reports it (uniform: every thread returns)
         // ---- this CTA's window, from a sample of its own rows
         const WinPlan P = window_plan(G, D, wcap);
-        fast_choose_window<D, A>(G, P, cx[0], cx[D > 1 ? 1 : 0], cx[D > 2 ? 2 : 0], cv, p0, nthr, npairs, HS, s_best,
-                                 s_origin, &s_exp);
+        // (or the one this CTA chose at an earlier execute of the handle: only speed
+        // depends on the window and the fixed-point scale, and sampling costs ~15 us)
+        if (reuse) {
+            if (threadIdx.x < 6) s_origin[threadIdx.x] = wcache[blockIdx.x * 8 + threadIdx.x];
+            if (threadIdx.x == 6) s_exp = (unsigned)wcache[blockIdx.x * 8 + 6];
+            __syncthreads();
+        } else {
+            fast_choose_window<D, A>(G, P, cx[0], cx[D > 1 ? 1 : 0], cx[D > 2 ? 2 : 0], cv, p0, nthr, npairs, HS,
+                                     s_best, s_origin, &s_exp);
+            if (threadIdx.x < 6) wcache[blockIdx.x * 8 + threadIdx.x] = s_origin[threadIdx.x];
+            if (threadIdx.x == 6) wcache[blockIdx.x * 8 + 6] = (int32_t)s_exp;
+        }
         c.W = 1;
 #pragma unroll
         for (int d = 0; d < D; ++d) {
@@ -397,7 +407,7 @@ bool fast_eligible(const Inputs &in, const Accum &acc, int ndim) {
 
 template <int D, int A, int SM, int MM>
 static cudaError_t launch_fast_t(const Geom &g, const Inputs &in, const Accum &acc, const LaunchCfg &lc, int smem,
-                                 int wcap, cudaStream_t s) {
+                                 int wcap, int32_t *wcache, int reuse, cudaStream_t s) {
     const int head = ((uintptr_t)in.ax[0] & 15u) ? 1 : 0;
     const uint32_t npairs = (uint32_t)((in.n - head) / 2);
     int blocks = lc.sms;  // one persistent CTA per SM: the whole shared memory holds the window
@@ -406,26 +416,27 @@ static cudaError_t launch_fast_t(const Geom &g, const Inputs &in, const Accum &a
     auto kern = k_bin_fast<D, A, SM, MM>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    kern<<<blocks, FAST_THREADS, smem, s>>>(g, in, acc, npairs, head, wcap);
+    kern<<<blocks, FAST_THREADS, smem, s>>>(g, in, acc, npairs, head, wcap, wcache, reuse);
     return cudaGetLastError();
 }
 
 template <int D>
 static cudaError_t launch_fast_d(const Geom &g, const Inputs &in, const Accum &acc, const LaunchCfg &lc, int smem,
-                                 int wcap, cudaStream_t s) {
-    if (in.nattr == 0 || !(acc.load_mask & 1u)) return launch_fast_t<D, 0, 0, 0>(g, in, acc, lc, smem, wcap, s);
+                                 int wcap, int32_t *wc, int reuse, cudaStream_t s) {
+    if (in.nattr == 0 || !(acc.load_mask & 1u))
+        return launch_fast_t<D, 0, 0, 0>(g, in, acc, lc, smem, wcap, wc, reuse, s);
     const bool sm = acc.sum_mask & 1u, mm = acc.mm_mask & 1u;
-    if (sm && mm) return launch_fast_t<D, 1, 1, 1>(g, in, acc, lc, smem, wcap, s);
-    if (sm) return launch_fast_t<D, 1, 1, 0>(g, in, acc, lc, smem, wcap, s);
-    return launch_fast_t<D, 1, 0, 1>(g, in, acc, lc, smem, wcap, s);
+    if (sm && mm) return launch_fast_t<D, 1, 1, 1>(g, in, acc, lc, smem, wcap, wc, reuse, s);
+    if (sm) return launch_fast_t<D, 1, 1, 0>(g, in, acc, lc, smem, wcap, wc, reuse, s);
+    return launch_fast_t<D, 1, 0, 1>(g, in, acc, lc, smem, wcap, wc, reuse, s);
 }
 
 cudaError_t launch_bin_fast(const Geom &g, const Inputs &in, const Accum &acc, const LaunchCfg &lc, int smem,
-                            int wcap, cudaStream_t s) {
+                            int wcap, int32_t *wcache, int reuse, cudaStream_t s) {
     switch (g.ndim) {
-    case 1: return launch_fast_d<1>(g, in, acc, lc, smem, wcap, s);
-    case 2: return launch_fast_d<2>(g, in, acc, lc, smem, wcap, s);
-    default: return launch_fast_d<3>(g, in, acc, lc, smem, wcap, s);
+    case 1: return launch_fast_d<1>(g, in, acc, lc, smem, wcap, wcache, reuse, s);
+    case 2: return launch_fast_d<2>(g, in, acc, lc, smem, wcap, wcache, reuse, s);
+    default: return launch_fast_d<3>(g, in, acc, lc, smem, wcap, wcache, reuse, s);
     }
 }
 

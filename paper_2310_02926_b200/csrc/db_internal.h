@@ -88,6 +88,7 @@ struct Meta {
     int32_t window[6];  // origin[3], extent[3]
     int32_t done;
     int32_t pad;
+    uint64_t trace[4];  // peer combine: %globaltimer at entry, after barrier A, last CTA done, after barrier B
 };
 
 struct Accum {
@@ -124,8 +125,10 @@ cudaError_t launch_bounds(const Geom &g, const Inputs &in, const Accum &acc, con
 cudaError_t launch_window(const Geom &g, const Inputs &in, const Accum &acc, int wcap, cudaStream_t s);
 cudaError_t launch_bin_general(const Geom &g, const Inputs &in, const Accum &acc, const LaunchCfg &lc, int smem,
                                cudaStream_t s);
+// wcache: per-CTA window + fixed-point exponent (8 ints per CTA) written when
+// reuse == 0, read instead of sampling when reuse != 0
 cudaError_t launch_bin_fast(const Geom &g, const Inputs &in, const Accum &acc, const LaunchCfg &lc, int smem,
-                            int wcap, cudaStream_t s);
+                            int wcap, int32_t *wcache, int reuse, cudaStream_t s);
 bool fast_eligible(const Inputs &in, const Accum &acc, int ndim);
 int fast_queue_bytes();
 cudaError_t launch_finalize(const Geom &g, const Accum &acc, Meta *meta_dev, int64_t n_rows_local,

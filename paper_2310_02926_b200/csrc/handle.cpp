@@ -24,7 +24,8 @@ struct Slot {
     unsigned char *base = nullptr;  // the slot's single device allocation (IPC-exported in peer mode)
     PeerSet peers{};
     Meta *meta_h = nullptr, *meta_d = nullptr;
-    cudaEvent_t done = nullptr, released = nullptr;
+    cudaEvent_t done = nullptr, released = nullptr, zeroed = nullptr;
+    bool used_before = false;  // a previous execute used this slot (its done event is valid)
     cudaEvent_t ev[EV_N] = {};
     bool recd[EV_N] = {};  // which events this execute recorded (profiling)
     bool prof_pending = false;
@@ -54,6 +55,7 @@ struct bin_handle {
     cudaStream_t side = nullptr;
     cudaStream_t meta_stream = nullptr;
     cudaStream_t copy = nullptr;  // staging copies (host, peer, snapshot)
+    cudaStream_t prep = nullptr;  // accumulator identities of the next slot (off the critical path)
     Slot slot[2];
     uint64_t next_ticket = 1;
     Stage stage[2][BIN_MAX_DIM + BIN_MAX_ATTR];
@@ -80,6 +82,9 @@ struct bin_handle {
     cudaEvent_t probe_ev = nullptr;
     bool probe_inflight = false;
     int since_probe = 0;
+    int32_t *wcache = nullptr;  // k_bin_fast per-CTA windows [sms][8] (reused across executes)
+    int64_t wcache_n = -1;
+    int64_t wcache_age = 0;
     unsigned char *part_base = nullptr;  // partition-route scratch (grown on demand)
     size_t part_bytes = 0;
     bool finalized = false;
@@ -93,6 +98,7 @@ static double route_coverage() {
     return e ? atof(e) : 0.5;
 }
 constexpr int ROUTE_REPROBE = 64;  // executes between asynchronous re-checks
+constexpr int WINDOW_RESAMPLE = 16;  // k_bin_fast executes between per-CTA window samples
 
 static int probe_route(const int32_t *p) {
     return (p[7] > 0 && (double)p[6] < route_coverage() * (double)p[7]) ? BIN_ROUTE_PARTITION : BIN_ROUTE_WINDOW;
@@ -157,6 +163,8 @@ static void free_slot(bin_handle *h, Slot &s) {
     s.meta_h = s.meta_d = nullptr;
     if (s.done) cudaEventDestroy(s.done);
     if (s.released) cudaEventDestroy(s.released);
+    if (s.zeroed) cudaEventDestroy(s.zeroed);
+    s.zeroed = nullptr;
     for (auto &e : s.ev)
         if (e) cudaEventDestroy(e), e = nullptr;
     s.done = s.released = nullptr;
@@ -212,6 +220,7 @@ static int alloc_slot(bin_handle *h, Slot &s) {
     s.meta_d = (Meta *)(base + o_meta);
     DB_CUDA(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
     DB_CUDA(cudaEventCreateWithFlags(&s.released, cudaEventDisableTiming));
+    DB_CUDA(cudaEventCreateWithFlags(&s.zeroed, cudaEventDisableTiming));
     for (auto &ev : s.ev) DB_CUDA(cudaEventCreate(&ev));
     return BIN_OK;
 }
@@ -434,6 +443,8 @@ int bin_init(const bin_spec_t *spec, const bin_placement_t *place, const bin_com
         return fail(cuda_error(ce, "cudaStreamCreate"));
     if ((ce = cudaStreamCreateWithFlags(&h->copy, cudaStreamNonBlocking)) != cudaSuccess)
         return fail(cuda_error(ce, "cudaStreamCreate"));
+    if ((ce = cudaStreamCreateWithFlags(&h->prep, cudaStreamNonBlocking)) != cudaSuccess)
+        return fail(cuda_error(ce, "cudaStreamCreate"));
     if (!h->spec.deterministic && h->spec.route == BIN_ROUTE_AUTO) {  // route probe buffers (executes allocate nothing)
         if ((ce = cudaMalloc(&h->probe_d, 64)) != cudaSuccess) return fail(cuda_error(ce, "cudaMalloc(probe)"));
         count_alloc(64);
@@ -464,6 +475,9 @@ int bin_init(const bin_spec_t *spec, const bin_placement_t *place, const bin_com
     h->smem_bytes = ((h->smem_bytes + 15) & ~15) + qbytes;
     for (auto &s : h->slot)
         if ((rc = alloc_slot(h, s))) return fail(rc);
+    if ((ce = cudaMalloc(&h->wcache, (size_t)h->lc.sms * 8 * sizeof(int32_t))) != cudaSuccess)
+        return fail(cuda_error(ce, "cudaMalloc(window cache)"));
+    count_alloc((int64_t)h->lc.sms * 32);
     for (auto &e : h->producer_ev)
         if ((ce = cudaEventCreateWithFlags(&e, cudaEventDisableTiming)) != cudaSuccess)
             return fail(cuda_error(ce, "cudaEventCreate"));
@@ -559,6 +573,7 @@ int bin_execute(bin_handle_t *h, bin_array_t *const *axes, int32_t naxes, bin_ar
         if (P.used && P.stream != s) DB_CUDA(cudaStreamWaitEvent(s, P.done, 0));
     }
     S.ticket = t;
+    S.used_before = S.used;
     S.used = true;
     S.meta_valid = false;
     S.stream = s;
@@ -676,11 +691,17 @@ int bin_execute(bin_handle_t *h, bin_array_t *const *axes, int32_t naxes, bin_ar
     // ---- a3: accumulator identities (+ the window choice when the bounds are manual
     // and the general kernel will run; k_bin_fast chooses its windows per CTA)
     bool fast = n > 0 && !h->spec.deterministic && !part && fast_eligible(in, S.acc, geom.ndim);
-    const bool window_in_prep = !geom.bounds_auto && !h->spec.deterministic && !fast && !part;
-    if ((e = launch_init(geom, in, S.acc, h->wcap, window_in_prep, s)) != cudaSuccess)
+    // a3 on the handle's prep stream: the slot's identities are written as soon
+    // as its previous execute is done (typically while the previous execute on
+    // the other slot is still binning), off the critical path; the work stream
+    // waits for them before its first kernel that touches the slot
+    if (S.used_before) DB_CUDA(cudaStreamWaitEvent(h->prep, S.done, 0));
+    if ((e = launch_init(geom, in, S.acc, h->wcap, false, h->prep)) != cudaSuccess)
         return cuda_error(e, "init kernel");
     S.launches++;
-    if ((rc = rec(EV_INIT1, true))) return rc;
+    DB_CUDA(cudaEventRecord(S.zeroed, h->prep));
+    DB_CUDA(cudaStreamWaitEvent(s, S.zeroed, 0));
+    const bool window_in_prep = !geom.bounds_auto && !h->spec.deterministic && !fast && !part;
     // ---- a2: automatic bounds (+ cross-rank Min, reading R3)
     if (geom.bounds_auto) {
         if ((e = launch_bounds(geom, in, S.acc, h->lc, s)) != cudaSuccess) return cuda_error(e, "bounds kernel");
@@ -715,7 +736,7 @@ int bin_execute(bin_handle_t *h, bin_array_t *const *axes, int32_t naxes, bin_ar
         variant = 3;
     } else {
         // ---- hot-window choice, then a4 + a5
-        const bool win_kernel = !window_in_prep && !fast && !part && n > 0;
+        const bool win_kernel = !fast && !part && n > 0;  // (window_in_prep: manual bounds, chosen here too)
         if (win_kernel) {
             if ((e = launch_window(geom, in, S.acc, h->wcap, s)) != cudaSuccess) return cuda_error(e, "window kernel");
             S.launches += 1;
@@ -733,7 +754,14 @@ int bin_execute(bin_handle_t *h, bin_array_t *const *axes, int32_t naxes, bin_ar
         } else {
             variant = ((uint64_t)h->wcap >= h->nbins ? 2 : 1) | (fast ? 16 : 0);
             if (n > 0) {
-                e = fast ? launch_bin_fast(geom, in, S.acc, h->lc, h->smem_bytes, h->wcap, s)
+                // per-CTA windows: sampled at the first fast execute and every
+                // WINDOW_RESAMPLE-th after it (and whenever the row count changes)
+                const bool reuse = fast && h->wcache_n == n && h->wcache_age % WINDOW_RESAMPLE != 0;
+                if (fast) {
+                    h->wcache_n = n;
+                    h->wcache_age = reuse ? h->wcache_age + 1 : 1;
+                }
+                e = fast ? launch_bin_fast(geom, in, S.acc, h->lc, h->smem_bytes, h->wcap, h->wcache, reuse ? 1 : 0, s)
                          : launch_bin_general(geom, in, S.acc, h->lc, h->smem_bytes, s);
                 if (e != cudaSuccess) return cuda_error(e, "bin kernel");
                 S.launches++, S.bin_launches++;
@@ -810,6 +838,13 @@ static int fetch_meta(bin_handle *h, Slot &S) {
     DB_CUDA(cudaMemcpyAsync(S.meta_h, S.meta_d, sizeof(Meta), cudaMemcpyDeviceToHost, h->meta_stream));
     DB_CUDA(cudaStreamSynchronize(h->meta_stream));
     S.meta_valid = true;
+    static const bool tr = getenv("DATABIN_TRACE") != nullptr;
+    if (tr && (S.meta_h->variant & 32)) {  // peer combine phase times on this rank (us)
+        const uint64_t *x = S.meta_h->trace;
+        fprintf(stderr, "[databin trace] rank %d ticket %llu: barrier A %.1f, slice %.1f, barrier B %.1f us\n",
+                h->rank, (unsigned long long)S.ticket, (x[1] - x[0]) * 1e-3, ((double)x[2] - (double)x[1]) * 1e-3,
+                ((double)x[3] - (double)x[2]) * 1e-3);
+    }
     return BIN_OK;
 }
 
@@ -921,6 +956,8 @@ int bin_finalize(bin_handle_t *h) {
                 if (e != cudaSuccess && rc == BIN_OK) rc = cuda_error(e, "bin_finalize");
             }
         if (h->side) cudaStreamSynchronize(h->side);
+        if (h->prep) cudaStreamSynchronize(h->prep);
+        if (h->copy) cudaStreamSynchronize(h->copy);
         for (void *p : h->opened) cudaIpcCloseMemHandle(p);
         h->opened.clear();
         if (h->flags) cudaFree(h->flags);
@@ -958,6 +995,11 @@ int bin_finalize(bin_handle_t *h) {
             h->probe_h = nullptr;
         }
         if (h->probe_ev) cudaEventDestroy(h->probe_ev), h->probe_ev = nullptr;
+        if (h->wcache) {
+            cudaFree(h->wcache);
+            count_free((int64_t)h->lc.sms * 32);
+            h->wcache = nullptr;
+        }
         if (h->gather) {
             cudaFree(h->gather);
             count_free((int64_t)h->gather_bytes);
@@ -970,6 +1012,11 @@ int bin_finalize(bin_handle_t *h) {
             cudaStreamDestroy(h->copy);
         }
         h->copy = nullptr;
+        if (h->prep) {
+            cudaStreamSynchronize(h->prep);
+            cudaStreamDestroy(h->prep);
+        }
+        h->prep = nullptr;
         h->side = nullptr;
         h->meta_stream = nullptr;
     }

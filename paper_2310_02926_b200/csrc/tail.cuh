@@ -66,6 +66,11 @@ constexpr long long SPIN_LIMIT_CYCLES = 4000000000ll;  // ~2 s
 __device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long ns;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+    return ns;
+}
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
     unsigned long long v;
     asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -84,6 +89,64 @@ __device__ __forceinline__ bool wait_all(const unsigned long long *flags, int nr
     return true;
 }
 
+// Common case (<= 1 summed and <= 1 min/max attribute, NR ranks): two bins
+// per thread with 16-byte accesses, and every load of them from every rank
+// issued before any store -- one NVLink round trip per pair of bins instead
+// of three (count, sum, min/max) per bin.
+template <int NR>
+__device__ __forceinline__ void combine_pair(const PeerSet &ps, uint64_t b, bool hs, bool hm) {
+    const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+    const double pinf = __longlong_as_double(0x7ff0000000000000ll);
+    const double ninf = __longlong_as_double((long long)0xfff0000000000000ull);
+    ulonglong2 c[NR], m0[NR], m1[NR];
+    double2 sv[NR];
+#pragma unroll
+    for (int p = 0; p < NR; ++p) {
+        c[p] = __ldcg((const ulonglong2 *)(ps.count[p] + b));
+        sv[p] = hs ? __ldcg((const double2 *)(ps.sum[p] + b)) : make_double2(0.0, 0.0);
+        m0[p] = hm ? __ldcg((const ulonglong2 *)ps.mm[p] + b) : make_ulonglong2(~0ull, ~0ull);
+        m1[p] = hm ? __ldcg((const ulonglong2 *)ps.mm[p] + b + 1) : make_ulonglong2(~0ull, ~0ull);
+    }
+    ulonglong2 cnt = make_ulonglong2(0ull, 0ull), mn = make_ulonglong2(~0ull, ~0ull), nx = mn;
+    double2 sm = make_double2(0.0, 0.0);  // rank-order fold from +0.0 (oracle partition mode)
+#pragma unroll
+    for (int p = 0; p < NR; ++p) {
+        cnt.x += c[p].x;
+        cnt.y += c[p].y;
+        sm.x = __dadd_rn(sm.x, sv[p].x);
+        sm.y = __dadd_rn(sm.y, sv[p].y);
+        mn.x = m0[p].x < mn.x ? m0[p].x : mn.x;
+        nx.x = m0[p].y < nx.x ? m0[p].y : nx.x;
+        mn.y = m1[p].x < mn.y ? m1[p].x : mn.y;
+        nx.y = m1[p].y < nx.y ? m1[p].y : nx.y;
+    }
+    const double2 avg = make_double2(cnt.x ? __ddiv_rn(sm.x, (double)cnt.x) : qnan,
+                                     cnt.y ? __ddiv_rn(sm.y, (double)cnt.y) : qnan);
+    const double2 vmin = make_double2(cnt.x ? dec_total(mn.x) : pinf, cnt.y ? dec_total(mn.y) : pinf);
+    const double2 vmax = make_double2(cnt.x ? dec_total(~nx.x) : ninf, cnt.y ? dec_total(~nx.y) : ninf);
+#pragma unroll
+    for (int q = 0; q < NR; ++q) {
+        *(ulonglong2 *)(ps.count[q] + b) = cnt;
+        if (hs) {
+            *(double2 *)(ps.sum[q] + b) = sm;
+            *(double2 *)(ps.oavg[q] + b) = avg;
+        }
+        if (hm) {
+            *(double2 *)(ps.omin[q] + b) = vmin;
+            *(double2 *)(ps.omax[q] + b) = vmax;
+        }
+    }
+}
+
+// the even-aligned pairs of bins in [s0, s1)
+template <int NR>
+__device__ __forceinline__ void combine_slice_fast(const PeerSet &ps, uint64_t s0, uint64_t s1, bool hs, bool hm) {
+    const uint64_t a0 = (s0 + 1) & ~1ull, a1 = s1 & ~1ull;
+    for (uint64_t b = a0 + 2 * ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x); b < a1;
+         b += 2 * (uint64_t)gridDim.x * blockDim.x)
+        combine_pair<NR>(ps, b, hs, hm);
+}
+
 __device__ __forceinline__ void combine_peer_body(const Geom &g, const PeerSet &ps, int rank, int nranks,
                                                   unsigned long long epoch, Meta *meta, int variant) {
     __shared__ bool ok_s, last_s;
@@ -92,10 +155,12 @@ __device__ __forceinline__ void combine_peer_body(const Geom &g, const PeerSet &
     // ---- barrier A: all partial accumulators complete
     if (threadIdx.x == 0) {
         if (blockIdx.x == 0) {
+            meta->trace[0] = globaltimer();
             __threadfence_system();
             for (int p = 0; p < nranks; ++p) st_release_sys(ps.flags[p] + rank, epoch);  // flagsA[rank] on peer p
         }
         ok_s = wait_all(ps.flags[rank], nranks, epoch);
+        if (blockIdx.x == 0) meta->trace[1] = globaltimer();
     }
     __syncthreads();
     const bool ok = ok_s;
@@ -105,8 +170,14 @@ __device__ __forceinline__ void combine_peer_body(const Geom &g, const PeerSet &
     const double qnan = __longlong_as_double(0x7ff8000000000000ll);
     const double pinf = __longlong_as_double(0x7ff0000000000000ll);
     const double ninf = __longlong_as_double((long long)0xfff0000000000000ull);
-    for (uint64_t b = s0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; ok && b < s1;
-         b += (uint64_t)gridDim.x * blockDim.x) {
+    // fast path: pairs of even-aligned bins (16-byte accesses need b even);
+    // the generic per-bin code takes the unpaired edge bins (<= 2) or all
+    const uint64_t e0 = (s0 + 1) & ~1ull, e1 = s1 & ~1ull;
+    const bool fastp = ok && nsum <= 1 && nmm <= 1 && (nranks == 2 || nranks == 4 || nranks == 8) && e0 < e1;
+    if (fastp && nranks == 2) combine_slice_fast<2>(ps, s0, s1, nsum == 1, nmm == 1);
+    else if (fastp && nranks == 4) combine_slice_fast<4>(ps, s0, s1, nsum == 1, nmm == 1);
+    else if (fastp && nranks == 8) combine_slice_fast<8>(ps, s0, s1, nsum == 1, nmm == 1);
+    auto generic = [&](uint64_t b) {
         unsigned long long cnt = 0;
         for (int p = 0; p < nranks; ++p) cnt += __ldcg(ps.count[p] + b);
         for (int q = 0; q < nranks; ++q) ps.count[q][b] = cnt;
@@ -132,6 +203,14 @@ __device__ __forceinline__ void combine_peer_body(const Geom &g, const PeerSet &
                 ps.omax[q][(uint64_t)s * B + b] = mx;
             }
         }
+    };
+    if (fastp) {
+        if (blockIdx.x == 0 && threadIdx.x == 0 && s0 < e0) generic(s0);
+        if (blockIdx.x == 0 && threadIdx.x == 1 && e1 < s1) generic(e1);
+    } else {
+        for (uint64_t b = s0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; ok && b < s1;
+             b += (uint64_t)gridDim.x * blockDim.x)
+            generic(b);
     }
     // ---- barrier B: every slice written everywhere
     __threadfence_system();
@@ -140,6 +219,7 @@ __device__ __forceinline__ void combine_peer_body(const Geom &g, const PeerSet &
     __syncthreads();
     if (!last_s) return;
     if (threadIdx.x == 0) {
+        meta->trace[2] = globaltimer();
         *ps.ctas_done = 0u;  // reset for the next execute (stream-ordered)
         __threadfence_system();
         for (int p = 0; p < nranks; ++p) st_release_sys(ps.flags[p] + 64 + rank, epoch);  // flagsB
@@ -162,6 +242,7 @@ __device__ __forceinline__ void combine_peer_body(const Geom &g, const PeerSet &
             meta->window[3 + d] = me.window[3 + d];
         }
         meta->done = 1;
+        meta->trace[3] = globaltimer();
         for (int a = 0; a < BIN_MAX_ATTR; ++a) me.fxexp[a] = 0u;
     }
 }
