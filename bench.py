@@ -322,6 +322,18 @@ def main():
         out_bytes = B * 8 * (1 + 4 * len(w.attrs))
         step_alg_bytes = bytes_per_row * N_total + out_bytes
         value = N_total / (ms_step * 1e-3)
+        var = int(prof.variant)
+        D = len(w.axes)
+        if var & 15 == 4:
+            kname = "partition route (k_part_keys, k_part_scan1/2, k_part_scatter[, k_part_refine], k_part_reduce)"
+        elif var & 15 == 3:
+            kname = "deterministic (k_det_keys, radix passes, k_det_segments, k_det_fold[_long])"
+        elif var & 16:
+            kname = f"k_bin_fast<{D},1,1,1>" if len(w.attrs) == 1 else f"k_bin_fast<{D},{len(w.attrs)},..>"
+        else:
+            kname = f"k_bin<{D},..>"
+        combine = ("fused NVLink peer-memory combine + finalize (k_combine_peer)" if var & 32
+                   else "NCCL allreduce of bin arrays + k_finalize") if world > 1 else "none (1 rank)"
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": args.scaling,
@@ -331,11 +343,11 @@ def main():
                        "axes": list(w.axes), "attrs": list(w.attrs), "ops": list(w.ops),
                        "exec": "lockstep (BIN_EXEC_SYNC, stream-ordered)", "deterministic": args.deterministic,
                        "l2": "inputs 24 B/row x rows >> 126 MB L2; no flush needed",
-                       "parallelism": f"dp{world} (row shards + NCCL allreduce of bin arrays)"},
+                       "parallelism": f"dp{world} (contiguous row shards per rank)", "combine": combine},
             "hbm": {"alg_bytes_per_step": step_alg_bytes,
                     "achieved_gbs_step": step_alg_bytes / (ms_step * 1e-3) / 1e9 / world,
                     "frac_of_8TBps_step": step_alg_bytes / (ms_step * 1e-3) / 1e9 / world / NOMINAL_HBM_GBS},
-            "roofline": {"bound": "hbm", "kernel": "k_bin (db::k_bin<2,1,true>)", "achieved": achieved,
+            "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved,
                          "peak": peak, "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": load_traffic(w.name), "ms_per_launch": ms_bin,
                          "alg_bytes_per_launch": alg_bytes_launch,
