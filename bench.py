@@ -2,13 +2,14 @@
 """Benchmark of the in situ DataBin hot path (arXiv 2310.02926, Sec. 4.2).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload c3|c2|c5] [--scaling strong|weak]
+                    [--workload c3|c2|c4|c5] [--scaling strong|weak] [--deterministic]
 
 Workload (default): BASELINE.json configs[2] -- 100M Plummer-clustered
 particles binned onto a 512x512 x-y mesh, count + sum/min/max/avg of mass,
-sharded across N GPUs (contiguous row blocks) with an NCCL allreduce of the
-bin arrays.  One "step" = one bin_execute over the rank's shard: accumulator
-init, window choice, bin kernel, cross-rank combine, finalize.  Inputs are
+sharded across N GPUs (contiguous row blocks); the bin arrays are combined
+over NVLink peer memory by one fused combine + finalize kernel (NCCL as the
+fallback).  One "step" = one bin_execute over the rank's shard: accumulator
+init, bin kernel(s), cross-rank combine, finalize.  Inputs are
 generated on the device by the seeded generator (synth/) before timing and
 are larger than L2 (2.4 GB vs 126 MB), so no L2 flush is needed.
 
@@ -172,7 +173,7 @@ def reference_arm(args):
     w = synth.CONFIGS[args.workload]
     import oracle
     oracle.build()
-    per_step = max(1.0, args.cpu_seconds / max(1, args.steps + args.warmup))
+    per_step = max(0.25, args.cpu_seconds / max(1, args.steps + args.warmup))  # K+W steps in ~a minute
     probe = cpu_baseline(w, per_step)
     n = int(probe["value"] * per_step)
     n = max(100_000, min(n, w.n))
