@@ -240,8 +240,17 @@ __device__ __forceinline__ void fast_choose_window(const DGeom G, const WinPlan 
 
 template <int D, int A, int SM, int MM>
 __global__ void __launch_bounds__(FAST_THREADS, 1)
-    k_bin_fast(Geom g, Inputs in, Accum acc, uint32_t npairs, int head, int wcap, int32_t *wcache, int reuse) {
+    k_bin_fast(Geom g, Inputs in, Accum acc, uint32_t npairs, int head, int wcap, int32_t *wcache, int reuse,
+               unsigned long long *ktrace) {
     constexpr bool HS = A == 1 && SM == 1, HM = A == 1 && MM == 1;
+    auto trace = [&](int k) {  // DATABIN_TRACE: per-CTA phase timestamps
+        if (ktrace && threadIdx.x == 0) {
+            unsigned long long ns;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+            ktrace[blockIdx.x * 4 + k] = ns;
+        }
+    };
+    trace(0);
     __shared__ unsigned long long s_best[FAST_THREADS / 32];
     __shared__ int s_origin[6];
     __shared__ unsigned s_exp;
@@ -319,6 +328,7 @@ __global__ void __launch_bounds__(FAST_THREADS, 1)
     uint32_t qn = 0;
     __syncthreads();
 
+    trace(1);
     uint32_t n_in = 0, rows = 0;
     for (uint32_t pb = p0 - lane; pb < npairs; pb += nthr) {  // warp-uniform trip count
         const uint32_t pc = pb + lane;
@@ -370,6 +380,7 @@ __global__ void __launch_bounds__(FAST_THREADS, 1)
         if (out_w) atomicAdd(&count[acc.nbins + 1], out_w);
     }
     __syncthreads();
+    trace(2);
 
     // flush the window into the global accumulator (L2 reductions)
     for (uint32_t l = threadIdx.x; l < W; l += FAST_THREADS) {
@@ -390,6 +401,10 @@ __global__ void __launch_bounds__(FAST_THREADS, 1)
             if (d != 0.0) atomicAdd(&sum[b], d);
         }
     }
+    if (ktrace) {
+        __syncthreads();
+        trace(3);
+    }
 }
 
 // Eligible: <= 1 attribute, bins < 2^29, 16-byte pairs (all columns in the same
@@ -407,7 +422,7 @@ bool fast_eligible(const Inputs &in, const Accum &acc, int ndim) {
 
 template <int D, int A, int SM, int MM>
 static cudaError_t launch_fast_t(const Geom &g, const Inputs &in, const Accum &acc, const LaunchCfg &lc, int smem,
-                                 int wcap, int32_t *wcache, int reuse, cudaStream_t s) {
+                                 int wcap, int32_t *wcache, int reuse, unsigned long long *ktrace, cudaStream_t s) {
     const int head = ((uintptr_t)in.ax[0] & 15u) ? 1 : 0;
     const uint32_t npairs = (uint32_t)((in.n - head) / 2);
     int blocks = lc.sms;  // one persistent CTA per SM: the whole shared memory holds the window
@@ -416,27 +431,27 @@ static cudaError_t launch_fast_t(const Geom &g, const Inputs &in, const Accum &a
     auto kern = k_bin_fast<D, A, SM, MM>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    kern<<<blocks, FAST_THREADS, smem, s>>>(g, in, acc, npairs, head, wcap, wcache, reuse);
+    kern<<<blocks, FAST_THREADS, smem, s>>>(g, in, acc, npairs, head, wcap, wcache, reuse, ktrace);
     return cudaGetLastError();
 }
 
 template <int D>
 static cudaError_t launch_fast_d(const Geom &g, const Inputs &in, const Accum &acc, const LaunchCfg &lc, int smem,
-                                 int wcap, int32_t *wc, int reuse, cudaStream_t s) {
+                                 int wcap, int32_t *wc, int reuse, unsigned long long *kt, cudaStream_t s) {
     if (in.nattr == 0 || !(acc.load_mask & 1u))
-        return launch_fast_t<D, 0, 0, 0>(g, in, acc, lc, smem, wcap, wc, reuse, s);
+        return launch_fast_t<D, 0, 0, 0>(g, in, acc, lc, smem, wcap, wc, reuse, kt, s);
     const bool sm = acc.sum_mask & 1u, mm = acc.mm_mask & 1u;
-    if (sm && mm) return launch_fast_t<D, 1, 1, 1>(g, in, acc, lc, smem, wcap, wc, reuse, s);
-    if (sm) return launch_fast_t<D, 1, 1, 0>(g, in, acc, lc, smem, wcap, wc, reuse, s);
-    return launch_fast_t<D, 1, 0, 1>(g, in, acc, lc, smem, wcap, wc, reuse, s);
+    if (sm && mm) return launch_fast_t<D, 1, 1, 1>(g, in, acc, lc, smem, wcap, wc, reuse, kt, s);
+    if (sm) return launch_fast_t<D, 1, 1, 0>(g, in, acc, lc, smem, wcap, wc, reuse, kt, s);
+    return launch_fast_t<D, 1, 0, 1>(g, in, acc, lc, smem, wcap, wc, reuse, kt, s);
 }
 
 cudaError_t launch_bin_fast(const Geom &g, const Inputs &in, const Accum &acc, const LaunchCfg &lc, int smem,
-                            int wcap, int32_t *wcache, int reuse, cudaStream_t s) {
+                            int wcap, int32_t *wcache, int reuse, unsigned long long *ktrace, cudaStream_t s) {
     switch (g.ndim) {
-    case 1: return launch_fast_d<1>(g, in, acc, lc, smem, wcap, wcache, reuse, s);
-    case 2: return launch_fast_d<2>(g, in, acc, lc, smem, wcap, wcache, reuse, s);
-    default: return launch_fast_d<3>(g, in, acc, lc, smem, wcap, wcache, reuse, s);
+    case 1: return launch_fast_d<1>(g, in, acc, lc, smem, wcap, wcache, reuse, ktrace, s);
+    case 2: return launch_fast_d<2>(g, in, acc, lc, smem, wcap, wcache, reuse, ktrace, s);
+    default: return launch_fast_d<3>(g, in, acc, lc, smem, wcap, wcache, reuse, ktrace, s);
     }
 }
 

@@ -40,8 +40,8 @@ cudaError_t launch_combine_peer(const Geom &g, const PeerSet &ps, int rank, int 
                                 Meta *meta, int variant, int deterministic, int sms, cudaStream_t s) {
     const uint64_t B = ps.me.nbins;
     const uint64_t slice = (B + nranks - 1) / nranks;
-    uint64_t blocks = (slice + COMB_THREADS - 1) / COMB_THREADS;
-    if (blocks > (uint64_t)sms * 4) blocks = (uint64_t)sms * 4;
+    uint64_t blocks = (slice * nranks + COMB_THREADS - 1) / COMB_THREADS;  // up to nranks lanes per bin
+    if (blocks > (uint64_t)sms * 8) blocks = (uint64_t)sms * 8;
     if (blocks < 1) blocks = 1;
     (void)deterministic;
     k_combine_peer<<<(unsigned)blocks, COMB_THREADS, 0, s>>>(g, ps, rank, nranks, epoch, meta, variant);

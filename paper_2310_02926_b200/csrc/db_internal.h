@@ -97,7 +97,7 @@ struct Accum {
     unsigned long long *mm;     // nmm * nbins * 2: {enc(min), ~enc(max)}
     unsigned long long *bounds; // 2*ndim: {enc(lo_d)..., ~enc(hi_d)...}
     int32_t *window;            // 6 ints: origin[3], extent[3]
-    uint32_t *whist;            // 4096 coarse-cell sample counts + [4096] last-CTA ticket (window choice)
+    uint32_t *sched;            // k_bin_fast tile counters [16][8] (zeroed by k_prep)
     uint32_t *fxexp;            // 16: max biased exponent of each summed attribute over the sample
     double *omin, *omax, *oavg; // outputs
     uint64_t nbins;
@@ -127,8 +127,10 @@ cudaError_t launch_bin_general(const Geom &g, const Inputs &in, const Accum &acc
                                cudaStream_t s);
 // wcache: per-CTA window + fixed-point exponent (8 ints per CTA) written when
 // reuse == 0, read instead of sampling when reuse != 0
+// ktrace (DATABIN_TRACE, else nullptr): per-CTA %globaltimer at start, loop
+// start, loop end, flush end (4 u64 per CTA)
 cudaError_t launch_bin_fast(const Geom &g, const Inputs &in, const Accum &acc, const LaunchCfg &lc, int smem,
-                            int wcap, int32_t *wcache, int reuse, cudaStream_t s);
+                            int wcap, int32_t *wcache, int reuse, unsigned long long *ktrace, cudaStream_t s);
 bool fast_eligible(const Inputs &in, const Accum &acc, int ndim);
 int fast_queue_bytes();
 cudaError_t launch_finalize(const Geom &g, const Accum &acc, Meta *meta_dev, int64_t n_rows_local,

@@ -83,6 +83,7 @@ struct bin_handle {
     bool probe_inflight = false;
     int since_probe = 0;
     int32_t *wcache = nullptr;  // k_bin_fast per-CTA windows [sms][8] (reused across executes)
+    unsigned long long *ktrace = nullptr;  // DATABIN_TRACE: k_bin_fast per-CTA phase timestamps [sms][4]
     int64_t wcache_n = -1;
     int64_t wcache_age = 0;
     unsigned char *part_base = nullptr;  // partition-route scratch (grown on demand)
@@ -179,8 +180,8 @@ static int alloc_slot(bin_handle *h, Slot &s) {
     size_t o_mm = o_sum + al(B * 8 * h->nsum);
     size_t o_bounds = o_mm + al(B * 16 * h->nmm);
     size_t o_window = o_bounds + al(6 * 8);
-    size_t o_whist = o_window + al(8 * 4);
-    size_t o_fxexp = o_whist + al(4097 * 4);
+    size_t o_sched = o_window + al(8 * 4);
+    size_t o_fxexp = o_sched + al(16 * 8 * 4);
     size_t o_omin = o_fxexp + al(16 * 4);
     size_t o_omax = o_omin + al(B * 8 * h->nmm);
     size_t o_oavg = o_omax + al(B * 8 * h->nmm);
@@ -201,7 +202,7 @@ static int alloc_slot(bin_handle *h, Slot &s) {
     s.acc.mm = (unsigned long long *)(base + o_mm);
     s.acc.bounds = (unsigned long long *)(base + o_bounds);
     s.acc.window = (int32_t *)(base + o_window);
-    s.acc.whist = (uint32_t *)(base + o_whist);
+    s.acc.sched = (uint32_t *)(base + o_sched);
     s.acc.fxexp = (uint32_t *)(base + o_fxexp);
     s.acc.omin = (double *)(base + o_omin);
     s.acc.omax = (double *)(base + o_omax);
@@ -478,6 +479,11 @@ int bin_init(const bin_spec_t *spec, const bin_placement_t *place, const bin_com
     if ((ce = cudaMalloc(&h->wcache, (size_t)h->lc.sms * 8 * sizeof(int32_t))) != cudaSuccess)
         return fail(cuda_error(ce, "cudaMalloc(window cache)"));
     count_alloc((int64_t)h->lc.sms * 32);
+    if (getenv("DATABIN_TRACE")) {
+        if ((ce = cudaMalloc(&h->ktrace, (size_t)h->lc.sms * 32)) != cudaSuccess)
+            return fail(cuda_error(ce, "cudaMalloc(trace)"));
+        cudaMemset(h->ktrace, 0, (size_t)h->lc.sms * 32);
+    }
     for (auto &e : h->producer_ev)
         if ((ce = cudaEventCreateWithFlags(&e, cudaEventDisableTiming)) != cudaSuccess)
             return fail(cuda_error(ce, "cudaEventCreate"));
@@ -761,7 +767,8 @@ int bin_execute(bin_handle_t *h, bin_array_t *const *axes, int32_t naxes, bin_ar
                     h->wcache_n = n;
                     h->wcache_age = reuse ? h->wcache_age + 1 : 1;
                 }
-                e = fast ? launch_bin_fast(geom, in, S.acc, h->lc, h->smem_bytes, h->wcap, h->wcache, reuse ? 1 : 0, s)
+                e = fast ? launch_bin_fast(geom, in, S.acc, h->lc, h->smem_bytes, h->wcap, h->wcache, reuse ? 1 : 0,
+                                           h->ktrace, s)
                          : launch_bin_general(geom, in, S.acc, h->lc, h->smem_bytes, s);
                 if (e != cudaSuccess) return cuda_error(e, "bin kernel");
                 S.launches++, S.bin_launches++;
@@ -839,6 +846,27 @@ static int fetch_meta(bin_handle *h, Slot &S) {
     DB_CUDA(cudaStreamSynchronize(h->meta_stream));
     S.meta_valid = true;
     static const bool tr = getenv("DATABIN_TRACE") != nullptr;
+    if (tr && h->ktrace && (S.meta_h->variant & 16)) {  // k_bin_fast per-CTA phases (us)
+        std::vector<unsigned long long> x((size_t)h->lc.sms * 4);
+        if (cudaMemcpy(x.data(), h->ktrace, x.size() * 8, cudaMemcpyDeviceToHost) == cudaSuccess) {
+            double t0 = 1e30, w = 0, lmin = 1e30, lmax = 0, f = 0, emin = 1e30, emax = 0;
+            for (int c = 0; c < h->lc.sms; ++c) {
+                const unsigned long long *q = &x[(size_t)c * 4];
+                if (!q[3]) continue;
+                t0 = fmin(t0, (double)q[0]);
+                w = fmax(w, (double)(q[1] - q[0]));
+                lmin = fmin(lmin, (double)(q[2] - q[1]));
+                lmax = fmax(lmax, (double)(q[2] - q[1]));
+                f = fmax(f, (double)(q[3] - q[2]));
+                emin = fmin(emin, (double)q[3]);
+                emax = fmax(emax, (double)q[3]);
+            }
+            fprintf(stderr, "[databin trace] rank %d ticket %llu k_bin_fast: prologue <= %.1f, loop %.1f..%.1f, "
+                            "flush <= %.1f, CTA end spread %.1f, total %.1f us\n", h->rank,
+                    (unsigned long long)S.ticket, w * 1e-3, lmin * 1e-3, lmax * 1e-3, f * 1e-3, (emax - emin) * 1e-3,
+                    (emax - t0) * 1e-3);
+        }
+    }
     if (tr && (S.meta_h->variant & 32)) {  // peer combine phase times on this rank (us)
         const uint64_t *x = S.meta_h->trace;
         fprintf(stderr, "[databin trace] rank %d ticket %llu: barrier A %.1f, slice %.1f, barrier B %.1f us\n",
@@ -995,6 +1023,7 @@ int bin_finalize(bin_handle_t *h) {
             h->probe_h = nullptr;
         }
         if (h->probe_ev) cudaEventDestroy(h->probe_ev), h->probe_ev = nullptr;
+        if (h->ktrace) cudaFree(h->ktrace), h->ktrace = nullptr;
         if (h->wcache) {
             cudaFree(h->wcache);
             count_free((int64_t)h->lc.sms * 32);

@@ -89,62 +89,51 @@ __device__ __forceinline__ bool wait_all(const unsigned long long *flags, int nr
     return true;
 }
 
-// Common case (<= 1 summed and <= 1 min/max attribute, NR ranks): two bins
-// per thread with 16-byte accesses, and every load of them from every rank
-// issued before any store -- one NVLink round trip per pair of bins instead
-// of three (count, sum, min/max) per bin.
+// Common case (<= 1 summed and <= 1 min/max attribute, NR ranks): NR lanes
+// per bin -- lane p loads rank p's partials, the group combines them with
+// shuffles (sum folded in rank order), and lane q stores the results into
+// rank q -- so a slice has NR x more requests in flight than a thread per bin
+// (the combine is bound by outstanding NVLink requests, not link bandwidth:
+// tools/microbench/peer_bench.cu).
 template <int NR>
-__device__ __forceinline__ void combine_pair(const PeerSet &ps, uint64_t b, bool hs, bool hm) {
+__device__ __forceinline__ void combine_slice_fast(const PeerSet &ps, uint64_t s0, uint64_t s1, bool hs, bool hm) {
     const double qnan = __longlong_as_double(0x7ff8000000000000ll);
     const double pinf = __longlong_as_double(0x7ff0000000000000ll);
     const double ninf = __longlong_as_double((long long)0xfff0000000000000ull);
-    ulonglong2 c[NR], m0[NR], m1[NR];
-    double2 sv[NR];
+    const unsigned lane = threadIdx.x & 31u, p = lane % NR;
+    const uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t span = (s1 - s0) * NR;
+    for (uint64_t t = t0; t - lane < span; t += nt) {  // warp-uniform trip count (shuffles below)
+        const bool valid = t < span;
+        const uint64_t b = s0 + (valid ? t / NR : 0);
+        const unsigned long long c = valid ? __ldcg(ps.count[p] + b) : 0ull;
+        const double sv = (valid && hs) ? __ldcg(ps.sum[p] + b) : 0.0;
+        const ulonglong2 m = (valid && hm) ? __ldcg((const ulonglong2 *)ps.mm[p] + b) : make_ulonglong2(~0ull, ~0ull);
+        unsigned long long cnt = c, mn = m.x, nx = m.y;
+        double sm = 0.0;  // rank-order fold from +0.0 (oracle partition mode)
+        const unsigned g0 = lane - p;
 #pragma unroll
-    for (int p = 0; p < NR; ++p) {
-        c[p] = __ldcg((const ulonglong2 *)(ps.count[p] + b));
-        sv[p] = hs ? __ldcg((const double2 *)(ps.sum[p] + b)) : make_double2(0.0, 0.0);
-        m0[p] = hm ? __ldcg((const ulonglong2 *)ps.mm[p] + b) : make_ulonglong2(~0ull, ~0ull);
-        m1[p] = hm ? __ldcg((const ulonglong2 *)ps.mm[p] + b + 1) : make_ulonglong2(~0ull, ~0ull);
-    }
-    ulonglong2 cnt = make_ulonglong2(0ull, 0ull), mn = make_ulonglong2(~0ull, ~0ull), nx = mn;
-    double2 sm = make_double2(0.0, 0.0);  // rank-order fold from +0.0 (oracle partition mode)
+        for (int q = 0; q < NR; ++q) sm = __dadd_rn(sm, __shfl_sync(0xffffffffu, sv, g0 + q));
 #pragma unroll
-    for (int p = 0; p < NR; ++p) {
-        cnt.x += c[p].x;
-        cnt.y += c[p].y;
-        sm.x = __dadd_rn(sm.x, sv[p].x);
-        sm.y = __dadd_rn(sm.y, sv[p].y);
-        mn.x = m0[p].x < mn.x ? m0[p].x : mn.x;
-        nx.x = m0[p].y < nx.x ? m0[p].y : nx.x;
-        mn.y = m1[p].x < mn.y ? m1[p].x : mn.y;
-        nx.y = m1[p].y < nx.y ? m1[p].y : nx.y;
-    }
-    const double2 avg = make_double2(cnt.x ? __ddiv_rn(sm.x, (double)cnt.x) : qnan,
-                                     cnt.y ? __ddiv_rn(sm.y, (double)cnt.y) : qnan);
-    const double2 vmin = make_double2(cnt.x ? dec_total(mn.x) : pinf, cnt.y ? dec_total(mn.y) : pinf);
-    const double2 vmax = make_double2(cnt.x ? dec_total(~nx.x) : ninf, cnt.y ? dec_total(~nx.y) : ninf);
-#pragma unroll
-    for (int q = 0; q < NR; ++q) {
-        *(ulonglong2 *)(ps.count[q] + b) = cnt;
+        for (int o = 1; o < NR; o <<= 1) {
+            cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+            const unsigned long long x = __shfl_xor_sync(0xffffffffu, mn, o);
+            const unsigned long long y = __shfl_xor_sync(0xffffffffu, nx, o);
+            mn = x < mn ? x : mn;
+            nx = y < nx ? y : nx;
+        }
+        if (!valid) continue;
+        const unsigned q = p;  // this lane stores into rank q
+        ps.count[q][b] = cnt;
         if (hs) {
-            *(double2 *)(ps.sum[q] + b) = sm;
-            *(double2 *)(ps.oavg[q] + b) = avg;
+            ps.sum[q][b] = sm;
+            ps.oavg[q][b] = cnt ? __ddiv_rn(sm, (double)cnt) : qnan;
         }
         if (hm) {
-            *(double2 *)(ps.omin[q] + b) = vmin;
-            *(double2 *)(ps.omax[q] + b) = vmax;
+            ps.omin[q][b] = cnt ? dec_total(mn) : pinf;
+            ps.omax[q][b] = cnt ? dec_total(~nx) : ninf;
         }
     }
-}
-
-// the even-aligned pairs of bins in [s0, s1)
-template <int NR>
-__device__ __forceinline__ void combine_slice_fast(const PeerSet &ps, uint64_t s0, uint64_t s1, bool hs, bool hm) {
-    const uint64_t a0 = (s0 + 1) & ~1ull, a1 = s1 & ~1ull;
-    for (uint64_t b = a0 + 2 * ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x); b < a1;
-         b += 2 * (uint64_t)gridDim.x * blockDim.x)
-        combine_pair<NR>(ps, b, hs, hm);
 }
 
 __device__ __forceinline__ void combine_peer_body(const Geom &g, const PeerSet &ps, int rank, int nranks,
@@ -170,10 +159,8 @@ __device__ __forceinline__ void combine_peer_body(const Geom &g, const PeerSet &
     const double qnan = __longlong_as_double(0x7ff8000000000000ll);
     const double pinf = __longlong_as_double(0x7ff0000000000000ll);
     const double ninf = __longlong_as_double((long long)0xfff0000000000000ull);
-    // fast path: pairs of even-aligned bins (16-byte accesses need b even);
-    // the generic per-bin code takes the unpaired edge bins (<= 2) or all
-    const uint64_t e0 = (s0 + 1) & ~1ull, e1 = s1 & ~1ull;
-    const bool fastp = ok && nsum <= 1 && nmm <= 1 && (nranks == 2 || nranks == 4 || nranks == 8) && e0 < e1;
+    // fast path (common case): NR lanes per bin; else the generic per-bin loop
+    const bool fastp = ok && nsum <= 1 && nmm <= 1 && (nranks == 2 || nranks == 4 || nranks == 8);
     if (fastp && nranks == 2) combine_slice_fast<2>(ps, s0, s1, nsum == 1, nmm == 1);
     else if (fastp && nranks == 4) combine_slice_fast<4>(ps, s0, s1, nsum == 1, nmm == 1);
     else if (fastp && nranks == 8) combine_slice_fast<8>(ps, s0, s1, nsum == 1, nmm == 1);
@@ -204,14 +191,10 @@ __device__ __forceinline__ void combine_peer_body(const Geom &g, const PeerSet &
             }
         }
     };
-    if (fastp) {
-        if (blockIdx.x == 0 && threadIdx.x == 0 && s0 < e0) generic(s0);
-        if (blockIdx.x == 0 && threadIdx.x == 1 && e1 < s1) generic(e1);
-    } else {
+    if (!fastp)
         for (uint64_t b = s0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; ok && b < s1;
              b += (uint64_t)gridDim.x * blockDim.x)
             generic(b);
-    }
     // ---- barrier B: every slice written everywhere
     __threadfence_system();
     __syncthreads();
