@@ -97,7 +97,6 @@ struct Accum {
     unsigned long long *mm;     // nmm * nbins * 2: {enc(min), ~enc(max)}
     unsigned long long *bounds; // 2*ndim: {enc(lo_d)..., ~enc(hi_d)...}
     int32_t *window;            // 6 ints: origin[3], extent[3]
-    uint32_t *sched;            // k_bin_fast tile counters [16][8] (zeroed by k_prep)
     uint32_t *fxexp;            // 16: max biased exponent of each summed attribute over the sample
     double *omin, *omax, *oavg; // outputs
     uint64_t nbins;

@@ -180,8 +180,7 @@ static int alloc_slot(bin_handle *h, Slot &s) {
     size_t o_mm = o_sum + al(B * 8 * h->nsum);
     size_t o_bounds = o_mm + al(B * 16 * h->nmm);
     size_t o_window = o_bounds + al(6 * 8);
-    size_t o_sched = o_window + al(8 * 4);
-    size_t o_fxexp = o_sched + al(16 * 8 * 4);
+    size_t o_fxexp = o_window + al(8 * 4);
     size_t o_omin = o_fxexp + al(16 * 4);
     size_t o_omax = o_omin + al(B * 8 * h->nmm);
     size_t o_oavg = o_omax + al(B * 8 * h->nmm);
@@ -202,7 +201,6 @@ static int alloc_slot(bin_handle *h, Slot &s) {
     s.acc.mm = (unsigned long long *)(base + o_mm);
     s.acc.bounds = (unsigned long long *)(base + o_bounds);
     s.acc.window = (int32_t *)(base + o_window);
-    s.acc.sched = (uint32_t *)(base + o_sched);
     s.acc.fxexp = (uint32_t *)(base + o_fxexp);
     s.acc.omin = (double *)(base + o_omin);
     s.acc.omax = (double *)(base + o_omax);

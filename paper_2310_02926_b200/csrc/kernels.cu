@@ -159,7 +159,6 @@ __global__ void __launch_bounds__(PREP_THREADS) k_prep(Geom g, Inputs in, Accum 
     const ulonglong2 ident = make_ulonglong2(~0ull, ~0ull);
     for (int64_t i = t0; i < (int64_t)(nb * acc.nmm); i += stride) ((ulonglong2 *)acc.mm)[i] = ident;
     if (t0 < 2 * g.ndim) acc.bounds[t0] = ~0ull;
-    if (t0 < 16 * 8) acc.sched[t0] = 0u;  // k_bin_fast tile counters
 }
 
 __global__ void __launch_bounds__(PREP_THREADS) k_window(Geom g, Inputs in, Accum acc, int wcap) {
