@@ -22,6 +22,7 @@
 // that exceeds ~2 s reports BIN_ENCCL instead of hanging.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "db_internal.h"
 #include "dev_common.cuh"
@@ -32,19 +33,35 @@ namespace db {
 constexpr int COMB_THREADS = 256;
 
 __global__ void __launch_bounds__(COMB_THREADS) k_combine_peer(Geom g, PeerSet ps, int rank, int nranks,
-                                                               unsigned long long epoch, Meta *meta, int variant) {
-    combine_peer_body(g, ps, rank, nranks, epoch, meta, variant);
+                                                               unsigned long long epoch, Meta *meta, int variant,
+                                                               int bulk) {
+    combine_peer_body(g, ps, rank, nranks, epoch, meta, variant, bulk != 0);
 }
+
+// dynamic shared memory of the bulk slice: NR ranks x 4 words + 5 output words per bin
+static size_t combine_bulk_smem(int nranks) { return ((size_t)nranks * 4 + 5) * COMB_CB * 8; }
 
 cudaError_t launch_combine_peer(const Geom &g, const PeerSet &ps, int rank, int nranks, unsigned long long epoch,
                                 Meta *meta, int variant, int deterministic, int sms, cudaStream_t s) {
     const uint64_t B = ps.me.nbins;
     const uint64_t slice = (B + nranks - 1) / nranks;
-    uint64_t blocks = (slice * nranks + COMB_THREADS - 1) / COMB_THREADS;  // up to nranks lanes per bin
-    if (blocks > (uint64_t)sms * 8) blocks = (uint64_t)sms * 8;
-    if (blocks < 1) blocks = 1;
     (void)deterministic;
-    k_combine_peer<<<(unsigned)blocks, COMB_THREADS, 0, s>>>(g, ps, rank, nranks, epoch, meta, variant);
+    static const bool no_bulk = getenv("DATABIN_COMBINE_BULK") && getenv("DATABIN_COMBINE_BULK")[0] == '0';
+    const bool bulk = !no_bulk && ps.me.nsum <= 1 && ps.me.nmm <= 1 && (nranks == 2 || nranks == 4 || nranks == 8);
+    uint64_t blocks;
+    size_t smem = 0;
+    if (bulk) {
+        smem = combine_bulk_smem(nranks);
+        cudaError_t e = cudaFuncSetAttribute(k_combine_peer, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        blocks = (slice + COMB_CB - 1) / COMB_CB;  // one chunk of COMB_CB bins per CTA and step
+        if (blocks > (uint64_t)sms * 2) blocks = (uint64_t)sms * 2;
+    } else {
+        blocks = (slice * nranks + COMB_THREADS - 1) / COMB_THREADS;  // up to nranks lanes per bin
+        if (blocks > (uint64_t)sms * 8) blocks = (uint64_t)sms * 8;
+    }
+    if (blocks < 1) blocks = 1;
+    k_combine_peer<<<(unsigned)blocks, COMB_THREADS, smem, s>>>(g, ps, rank, nranks, epoch, meta, variant, bulk ? 1 : 0);
     return cudaGetLastError();
 }
 

@@ -136,8 +136,121 @@ __device__ __forceinline__ void combine_slice_fast(const PeerSet &ps, uint64_t s
     }
 }
 
+// ---- TMA bulk-copy slice (cp.async.bulk): each CTA takes chunks of CB bins of
+// the slice; one thread pulls every rank's count/sum/min-max chunk into
+// shared memory (one mbarrier), the CTA reduces and finalizes there, and one
+// thread pushes the five output chunks to every rank with bulk stores.  Bulk
+// copies move 4-8 KB per request instead of 8-16 B per lane, so the slice is
+// no longer bound by SM-issued NVLink requests.  Shared memory (u64 words):
+// in [NR][count CB | sum CB | mm 2CB], out [count | sum | avg | min | max][CB].
+constexpr uint32_t COMB_CB = 512;
+
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src), "r"(bytes),
+                 "r"((unsigned)__cvta_generic_to_shared(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void *dst, const void *src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                 ::"l"(dst), "r"((unsigned)__cvta_generic_to_shared(src)), "r"(bytes)
+                 : "memory");
+}
+
+template <int NR>
+__device__ void combine_slice_bulk(const PeerSet &ps, uint64_t e0, uint64_t e1, bool hs, bool hm) {
+    extern __shared__ __align__(128) unsigned long long cb_smem[];
+    __shared__ __align__(8) uint64_t bar;
+    constexpr uint32_t CB = COMB_CB, IN = 4 * CB;  // u64 words per rank
+    unsigned long long *in = cb_smem, *out = cb_smem + NR * IN;
+    const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+    const double pinf = __longlong_as_double(0x7ff0000000000000ll);
+    const double ninf = __longlong_as_double((long long)0xfff0000000000000ull);
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((unsigned)__cvta_generic_to_shared(&bar)) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    uint32_t parity = 0;
+    const uint64_t nch = (e1 - e0 + CB - 1) / CB;
+    for (uint64_t ch = blockIdx.x; ch < nch; ch += gridDim.x) {
+        const uint64_t b0 = e0 + ch * CB;
+        const uint32_t nb = (uint32_t)min((uint64_t)CB, e1 - b0);  // even
+        if (threadIdx.x == 0) {
+            const uint32_t bytes = NR * nb * 8u * (1u + (hs ? 1u : 0u) + (hm ? 2u : 0u));
+            unsigned long long st;
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 %0, [%1], %2;"
+                         : "=l"(st) : "r"((unsigned)__cvta_generic_to_shared(&bar)), "r"(bytes) : "memory");
+            (void)st;
+#pragma unroll
+            for (int p = 0; p < NR; ++p) {
+                bulk_g2s(in + p * IN, ps.count[p] + b0, nb * 8u, &bar);
+                if (hs) bulk_g2s(in + p * IN + CB, ps.sum[p] + b0, nb * 8u, &bar);
+                if (hm) bulk_g2s(in + p * IN + 2 * CB, ps.mm[p] + 2 * b0, nb * 16u, &bar);
+            }
+        }
+        {  // wait for the chunk (all threads)
+            unsigned done = 0;
+            while (!done) {
+                asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                             : "=r"(done) : "r"((unsigned)__cvta_generic_to_shared(&bar)), "r"(parity) : "memory");
+            }
+            parity ^= 1u;
+        }
+        for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) {
+            unsigned long long cnt = 0, mn = ~0ull, nx = ~0ull;
+            double sm = 0.0;  // rank-order fold from +0.0 (oracle partition mode)
+#pragma unroll
+            for (int p = 0; p < NR; ++p) {
+                const unsigned long long *q = in + p * IN;
+                cnt += q[i];
+                if (hs) sm = __dadd_rn(sm, __longlong_as_double((long long)q[CB + i]));
+                if (hm) {
+                    const unsigned long long a = q[2 * CB + 2 * i], b = q[2 * CB + 2 * i + 1];
+                    mn = a < mn ? a : mn;
+                    nx = b < nx ? b : nx;
+                }
+            }
+            out[i] = cnt;
+            if (hs) {
+                out[CB + i] = (unsigned long long)__double_as_longlong(sm);
+                out[2 * CB + i] = (unsigned long long)__double_as_longlong(cnt ? __ddiv_rn(sm, (double)cnt) : qnan);
+            }
+            if (hm) {
+                out[3 * CB + i] = (unsigned long long)__double_as_longlong(cnt ? dec_total(mn) : pinf);
+                out[4 * CB + i] = (unsigned long long)__double_as_longlong(cnt ? dec_total(~nx) : ninf);
+            }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy writes -> bulk copies
+        __syncthreads();
+        if (threadIdx.x == 0) {
+#pragma unroll
+            for (int q = 0; q < NR; ++q) {
+                bulk_s2g(ps.count[q] + b0, out, nb * 8u);
+                if (hs) {
+                    bulk_s2g(ps.sum[q] + b0, out + CB, nb * 8u);
+                    bulk_s2g(ps.oavg[q] + b0, out + 2 * CB, nb * 8u);
+                }
+                if (hm) {
+                    bulk_s2g(ps.omin[q] + b0, out + 3 * CB, nb * 8u);
+                    bulk_s2g(ps.omax[q] + b0, out + 4 * CB, nb * 8u);
+                }
+            }
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // smem reusable
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {  // writes performed, and ordered before the generic-proxy flag stores
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+    }
+}
+
+// bulk: the slice uses TMA bulk copies (the kernel was launched with
+// combine_bulk_smem(nranks) bytes of dynamic shared memory)
 __device__ __forceinline__ void combine_peer_body(const Geom &g, const PeerSet &ps, int rank, int nranks,
-                                                  unsigned long long epoch, Meta *meta, int variant) {
+                                                  unsigned long long epoch, Meta *meta, int variant, bool bulk) {
     __shared__ bool ok_s, last_s;
     const Accum &me = ps.me;
     const uint64_t B = me.nbins;
@@ -159,11 +272,6 @@ __device__ __forceinline__ void combine_peer_body(const Geom &g, const PeerSet &
     const double qnan = __longlong_as_double(0x7ff8000000000000ll);
     const double pinf = __longlong_as_double(0x7ff0000000000000ll);
     const double ninf = __longlong_as_double((long long)0xfff0000000000000ull);
-    // fast path (common case): NR lanes per bin; else the generic per-bin loop
-    const bool fastp = ok && nsum <= 1 && nmm <= 1 && (nranks == 2 || nranks == 4 || nranks == 8);
-    if (fastp && nranks == 2) combine_slice_fast<2>(ps, s0, s1, nsum == 1, nmm == 1);
-    else if (fastp && nranks == 4) combine_slice_fast<4>(ps, s0, s1, nsum == 1, nmm == 1);
-    else if (fastp && nranks == 8) combine_slice_fast<8>(ps, s0, s1, nsum == 1, nmm == 1);
     auto generic = [&](uint64_t b) {
         unsigned long long cnt = 0;
         for (int p = 0; p < nranks; ++p) cnt += __ldcg(ps.count[p] + b);
@@ -191,6 +299,25 @@ __device__ __forceinline__ void combine_peer_body(const Geom &g, const PeerSet &
             }
         }
     };
+    // fast path (common case): NR lanes per bin; else the generic per-bin loop
+    const bool fastp = ok && nsum <= 1 && nmm <= 1 && (nranks == 2 || nranks == 4 || nranks == 8);
+    if (bulk && fastp) {  // TMA bulk copies for the even-aligned body; the <= 2 edge bins below
+        const uint64_t e0 = (s0 + 1) & ~1ull, e1 = s1 & ~1ull;
+        if (e0 < e1) {
+            if (nranks == 2) combine_slice_bulk<2>(ps, e0, e1, nsum == 1, nmm == 1);
+            else if (nranks == 4) combine_slice_bulk<4>(ps, e0, e1, nsum == 1, nmm == 1);
+            else combine_slice_bulk<8>(ps, e0, e1, nsum == 1, nmm == 1);
+        }
+        if (blockIdx.x == 0 && threadIdx.x < 2) {
+            const uint64_t b = threadIdx.x == 0 ? s0 : e1;
+            const bool edge = threadIdx.x == 0 ? (e0 < e1 ? s0 < e0 : false) : (e0 < e1 ? e1 < s1 : false);
+            if (edge) generic(b);
+            if (threadIdx.x == 0 && !(e0 < e1))
+                for (uint64_t bb = s0; bb < s1; ++bb) generic(bb);
+        }
+    } else if (fastp && nranks == 2) combine_slice_fast<2>(ps, s0, s1, nsum == 1, nmm == 1);
+    else if (fastp && nranks == 4) combine_slice_fast<4>(ps, s0, s1, nsum == 1, nmm == 1);
+    else if (fastp && nranks == 8) combine_slice_fast<8>(ps, s0, s1, nsum == 1, nmm == 1);
     if (!fastp)
         for (uint64_t b = s0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; ok && b < s1;
              b += (uint64_t)gridDim.x * blockDim.x)
