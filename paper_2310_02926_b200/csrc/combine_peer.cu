@@ -55,7 +55,7 @@ cudaError_t launch_combine_peer(const Geom &g, const PeerSet &ps, int rank, int 
         cudaError_t e = cudaFuncSetAttribute(k_combine_peer, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         blocks = (slice + COMB_CB - 1) / COMB_CB;  // one chunk of COMB_CB bins per CTA and step
-        if (blocks > (uint64_t)sms * 2) blocks = (uint64_t)sms * 2;
+        if (blocks > (uint64_t)sms * 4) blocks = (uint64_t)sms * 4;
     } else {
         blocks = (slice * nranks + COMB_THREADS - 1) / COMB_THREADS;  // up to nranks lanes per bin
         if (blocks > (uint64_t)sms * 8) blocks = (uint64_t)sms * 8;

@@ -143,7 +143,10 @@ __device__ __forceinline__ void combine_slice_fast(const PeerSet &ps, uint64_t s
 // copies move 4-8 KB per request instead of 8-16 B per lane, so the slice is
 // no longer bound by SM-issued NVLink requests.  Shared memory (u64 words):
 // in [NR][count CB | sum CB | mm 2CB], out [count | sum | avg | min | max][CB].
-constexpr uint32_t COMB_CB = 512;
+#ifndef BIN_COMB_CB
+#define BIN_COMB_CB 256
+#endif
+constexpr uint32_t COMB_CB = BIN_COMB_CB;  // bins per chunk (2 x 256 B per array per rank)
 
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
