@@ -285,6 +285,73 @@ const char *bin_last_error(void);
 /* Library version string. */
 const char *bin_version(void);
 
+/* ---- fused multi-operator binning ----
+ * The paper's in situ step applies the DataBin operator "to 10 variables over
+ * 9 coordinate systems for a total of 90 binning operations", each coordinate
+ * system "done sequentially in a separate data binning operator instance"
+ * (PAPER.md:511-514).  A bin_multi_t runs K such instances over ONE shared
+ * list of columns as a single fused launch sequence: one identity kernel for
+ * all K accumulators, one bounds kernel for every auto-bounded axis column,
+ * one accumulate kernel that reads each row's columns once and updates all K
+ * meshes, [the cross-rank combine of all K: three NCCL allreduces], one
+ * finalize kernel for all K.  Per instance the result is the one a separate
+ * bin_init/bin_execute of the same spec gives (same definition, same
+ * readings R1-R17; counts/min/max bit-identical, sums within reading R8).
+ *
+ * bin_multi_op_t: spec = the instance's mesh, bounds and reductions
+ *   (deterministic must be 0 -> else BIN_ENOTSUP; route is ignored);
+ *   axis_col[d] / attr_col[a] = indices into the column list given to
+ *   bin_multi_execute (0 <= index < ncols; a column may serve any number of
+ *   instances, as axis or attribute).
+ * Limits: 1 <= nops <= BIN_MULTI_MAX_OPS, 1 <= ncols <= BIN_MULTI_MAX_COLS. */
+#define BIN_MULTI_MAX_OPS 32
+#define BIN_MULTI_MAX_COLS 16
+typedef struct {
+    bin_spec_t spec;
+    int32_t axis_col[BIN_MAX_DIM];
+    int32_t attr_col[BIN_MAX_ATTR];
+} bin_multi_op_t;
+typedef struct bin_multi bin_multi_t; /* opaque */
+
+/* Creates the fused instance set: validates every spec and column index
+ * (BIN_EINVAL / BIN_ENOTSUP as bin_init), resolves the device by Eq. (1),
+ * allocates two result slots holding all K accumulators (type-major: all
+ * counts, all sums, all min/max, so a multi-rank combine is three NCCL
+ * allreduces), creates the NCCL communicator when comm->nranks > 1.
+ * ops is copied; the caller keeps ownership. */
+int bin_multi_init(const bin_multi_op_t *ops, int32_t nops, int32_t ncols, const bin_placement_t *place,
+                   const bin_comm_t *comm, bin_multi_t **out);
+
+/* Bins one batch of rows through all K instances.  cols[0..ncols) are
+ * equal-length f64 columns; device-resident columns on the analysis device
+ * are read in place (zero copy), others are staged on the copy stream (host
+ * memory: H2D; another GPU: NVLink peer copy).  Work is stream-ordered after
+ * each column's producer stream.  Returns after enqueue (lockstep SYNC with a
+ * BIN_SYNC first column blocks until done, as bin_execute).  Results of a
+ * ticket stay valid until the second following execute.
+ * Errors: BIN_ESHAPE (ncols or lengths), BIN_EDTYPE, BIN_ENOMEM, BIN_ECUDA, BIN_ENCCL. */
+int bin_multi_execute(bin_multi_t *m, bin_array_t *const *cols, int32_t ncols, uint64_t *ticket);
+
+/* Blocks until `ticket` is done; BIN_EDEGENERATE if any auto-bounded
+ * instance saw no finite rows. */
+int bin_multi_wait(bin_multi_t *m, uint64_t ticket);
+
+/* Waits, then fills *out with instance `op`'s result (library-owned device
+ * pointers, same layout and sentinels as bin_result).  BIN_EINVAL for op out
+ * of range. */
+int bin_multi_result(bin_multi_t *m, uint64_t ticket, int32_t op, bin_result_t *out);
+
+/* Profiling of the fused sequence (ms_init, ms_bounds, ms_bin, ms_combine,
+ * ms_finalize, executes, kernel_launches; variant = 64). */
+int bin_multi_profile_enable(bin_multi_t *m, int32_t on);
+int bin_multi_profile_read(bin_multi_t *m, bin_profile_t *out);
+
+/* The stream the last execute was enqueued on. */
+int bin_multi_stream(bin_multi_t *m, bin_stream_t *stream);
+
+/* Drains, frees everything, destroys the communicator.  NULL is a no-op. */
+int bin_multi_finalize(bin_multi_t *m);
+
 #ifdef __cplusplus
 }
 #endif

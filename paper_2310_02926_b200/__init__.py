@@ -19,7 +19,7 @@ from .capi import (  # noqa: F401
     BIN_ALLOC_HOST_PINNED, BIN_ASYNC, BIN_DEVICE_AUTO, BIN_DEVICE_HOST, BIN_EXEC_ASYNC, BIN_EXEC_PEER,
     BIN_EXEC_SYNC, BIN_F64, BIN_OP_AVG, BIN_OP_MAX, BIN_OP_MIN, BIN_OP_SUM, BIN_ROUTE_AUTO, BIN_ROUTE_PARTITION,
     BIN_ROUTE_WINDOW, BIN_SYNC, EXPORTED, OPS, ROUTES,
-    RELEASE_FN, BinError, bin_comm_t, bin_placement_t, bin_profile_t, bin_result_t, bin_spec_t, check, lib)
+    BIN_MULTI_MAX_COLS, BIN_MULTI_MAX_OPS, RELEASE_FN, BinError, bin_comm_t, bin_multi_op_t, bin_placement_t, bin_profile_t, bin_result_t, bin_spec_t, check, lib)
 
 _lib = lib()  # load (and build if stale) at import: no silent fallback
 
@@ -201,6 +201,70 @@ def bin_version() -> str:
     return _lib.bin_version().decode()
 
 
+# ---------------------------------------------------------------- fused multi-operator (bin_multi_*)
+def make_multi_op(spec: bin_spec_t, axis_col, attr_col=()) -> bin_multi_op_t:
+    """One instance of a fused set: its spec plus indices into the shared column list."""
+    o = bin_multi_op_t()
+    o.spec = spec
+    for d, c in enumerate(axis_col):
+        o.axis_col[d] = int(c)
+    for a, c in enumerate(attr_col):
+        o.attr_col[a] = int(c)
+    return o
+
+
+def bin_multi_init(ops, ncols, placement=None, rank=0, nranks=1, nccl_id: bytes | None = None):
+    arr = (bin_multi_op_t * len(ops))(*ops)
+    comm = bin_comm_t()
+    comm.rank, comm.nranks = rank, nranks
+    idbuf = None
+    if nccl_id is not None:
+        idbuf = ctypes.create_string_buffer(nccl_id, 128)
+        comm.nccl_unique_id = ctypes.cast(idbuf, ctypes.c_void_p)
+    out = ctypes.c_void_p()
+    pl = ctypes.byref(placement) if placement is not None else None
+    check(_lib.bin_multi_init(arr, len(ops), int(ncols), pl, ctypes.byref(comm), ctypes.byref(out)),
+          "bin_multi_init")
+    return out.value
+
+
+def bin_multi_execute(m, cols):
+    c = (ctypes.c_void_p * max(1, len(cols)))(*cols)
+    t = ctypes.c_uint64()
+    check(_lib.bin_multi_execute(ctypes.c_void_p(m), c, len(cols), ctypes.byref(t)), "bin_multi_execute")
+    return t.value
+
+
+def bin_multi_wait(m, ticket):
+    check(_lib.bin_multi_wait(ctypes.c_void_p(m), ticket), "bin_multi_wait")
+
+
+def bin_multi_result(m, ticket, op) -> bin_result_t:
+    r = bin_result_t()
+    check(_lib.bin_multi_result(ctypes.c_void_p(m), ticket, int(op), ctypes.byref(r)), "bin_multi_result")
+    return r
+
+
+def bin_multi_profile_enable(m, on=True):
+    check(_lib.bin_multi_profile_enable(ctypes.c_void_p(m), int(bool(on))), "bin_multi_profile_enable")
+
+
+def bin_multi_profile_read(m) -> bin_profile_t:
+    p = bin_profile_t()
+    check(_lib.bin_multi_profile_read(ctypes.c_void_p(m), ctypes.byref(p)), "bin_multi_profile_read")
+    return p
+
+
+def bin_multi_stream(m):
+    s = ctypes.c_void_p()
+    check(_lib.bin_multi_stream(ctypes.c_void_p(m), ctypes.byref(s)), "bin_multi_stream")
+    return s.value or 0
+
+
+def bin_multi_finalize(m):
+    check(_lib.bin_multi_finalize(ctypes.c_void_p(m)), "bin_multi_finalize")
+
+
 # ---------------------------------------------------------------- marshalling helpers
 def wrap_tensor(t, stream=None, mode=BIN_ASYNC):
     """Zero-copy bin_array for a contiguous float64 torch tensor (borrowed)."""
@@ -219,9 +283,10 @@ def wrap_numpy(a: np.ndarray, mode=BIN_SYNC):
     return bin_array_wrap(a.ctypes.data, a.shape[0], -1, BIN_ALLOC_HOST, 0, mode), a
 
 
-def result_to_numpy(h, ticket, spec: bin_spec_t) -> dict:
-    """Copies one execute's outputs to host numpy arrays (D2H through bin_copy)."""
-    r = bin_result(h, ticket)
+def result_to_numpy(h, ticket, spec: bin_spec_t, op=None) -> dict:
+    """Copies one execute's outputs to host numpy arrays (D2H through bin_copy).
+    With ``op`` set, ``h`` is a bin_multi handle and instance ``op`` is read."""
+    r = bin_result(h, ticket) if op is None else bin_multi_result(h, ticket, op)
     B = int(r.nbins)
     out = dict(n_in=int(r.n_in), n_out=int(r.n_out), lo=np.array(r.lo[:spec.ndim]),
                hi=np.array(r.hi[:spec.ndim]), device=r.device)

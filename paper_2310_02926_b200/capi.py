@@ -68,6 +68,13 @@ class bin_profile_t(ctypes.Structure):
                 ("bin_launches", ctypes.c_int64), ("variant", ctypes.c_int32), ("window", ctypes.c_int32 * 3)]
 
 
+BIN_MULTI_MAX_OPS, BIN_MULTI_MAX_COLS = 32, 16
+
+
+class bin_multi_op_t(ctypes.Structure):
+    _fields_ = [("spec", bin_spec_t), ("axis_col", ctypes.c_int32 * 3), ("attr_col", ctypes.c_int32 * 16)]
+
+
 RELEASE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p)
 
 _P = ctypes.POINTER
@@ -96,6 +103,15 @@ _SIGS = {
     "bin_finalize": (ctypes.c_int, [_vp]),
     "bin_nccl_unique_id": (ctypes.c_int, [_vp]),
     "bin_copy": (ctypes.c_int, [_vp, _vp, ctypes.c_uint64, _vp]),
+    "bin_multi_init": (ctypes.c_int, [_P(bin_multi_op_t), ctypes.c_int32, ctypes.c_int32, _P(bin_placement_t),
+                                      _P(bin_comm_t), _P(_vp)]),
+    "bin_multi_execute": (ctypes.c_int, [_vp, _P(_vp), ctypes.c_int32, _P(ctypes.c_uint64)]),
+    "bin_multi_wait": (ctypes.c_int, [_vp, ctypes.c_uint64]),
+    "bin_multi_result": (ctypes.c_int, [_vp, ctypes.c_uint64, ctypes.c_int32, _P(bin_result_t)]),
+    "bin_multi_profile_enable": (ctypes.c_int, [_vp, ctypes.c_int32]),
+    "bin_multi_profile_read": (ctypes.c_int, [_vp, _P(bin_profile_t)]),
+    "bin_multi_stream": (ctypes.c_int, [_vp, _P(_vp)]),
+    "bin_multi_finalize": (ctypes.c_int, [_vp]),
     "bin_last_error": (ctypes.c_char_p, []),
     "bin_version": (ctypes.c_char_p, []),
 }

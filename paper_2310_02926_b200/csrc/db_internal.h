@@ -20,6 +20,9 @@ int cuda_error(cudaError_t e, const char *what);
         if (e_ != cudaSuccess) return ::db::cuda_error(e_, #expr); \
     } while (0)
 
+// checks one bin_spec_t (BIN_EINVAL / BIN_ENOTSUP with a message), *nbins = prod(res)
+int validate_spec(const bin_spec_t *sp, uint64_t *nbins);
+
 // ---------------------------------------------------------------- allocator
 void *dev_alloc(size_t bytes, int device, cudaStream_t stream, bool async);
 void dev_free(void *p, int device, cudaStream_t stream, bool async);
@@ -194,4 +197,29 @@ void free_det_scratch(DetScratch &ds);
 cudaError_t launch_rank_fold(const double *gathered, int nranks, uint64_t len, double *sum, int sms, cudaStream_t s);
 int ensure_det_scratch(DetScratch &ds, int64_t n, uint64_t nbins, int device, int sms);
 
+
+// fused multi-operator binning (multi.cu): K instances over one column list
+constexpr int MULTI_MAX_OPS = BIN_MULTI_MAX_OPS;
+constexpr int MULTI_MAX_COLS = BIN_MULTI_MAX_COLS;
+struct MultiOp {
+    Geom g;
+    Accum acc;   // count/sum/mm/bounds/outputs of this instance inside the slot allocation
+    Meta *meta;  // device
+    int32_t axc[3];
+    int32_t atc[BIN_MAX_ATTR];
+    int32_t nattr;
+};
+struct MultiArgs {
+    const double *col[MULTI_MAX_COLS];
+    int64_t n;
+    int32_t ncols, nops;
+    int32_t k0, k1;         // instances [k0, k1) of this accumulate launch (L2-sized group)
+    uint32_t used_cols;     // columns any instance reads
+    uint32_t bound_cols;    // columns some auto-bounded instance takes bounds of
+    const MultiOp *ops;     // device array [nops]
+};
+cudaError_t launch_multi_init(const MultiArgs &a, uint64_t max_work, cudaStream_t s);
+cudaError_t launch_multi_bounds(const MultiArgs &a, const LaunchCfg &lc, cudaStream_t s);
+cudaError_t launch_multi_bin(const MultiArgs &a, const LaunchCfg &lc, cudaStream_t s);
+cudaError_t launch_multi_finalize(const MultiArgs &a, uint64_t max_bins, cudaStream_t s);
 }  // namespace db

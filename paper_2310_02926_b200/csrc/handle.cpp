@@ -224,7 +224,7 @@ static int alloc_slot(bin_handle *h, Slot &s) {
     return BIN_OK;
 }
 
-static int validate_spec(const bin_spec_t *sp, uint64_t *nbins) {
+int db::validate_spec(const bin_spec_t *sp, uint64_t *nbins) {
     if (sp->ndim < 1 || sp->ndim > BIN_MAX_DIM) return set_error(BIN_ENOTSUP, "ndim %d not in 1..3", sp->ndim);
     if (sp->nattr < 0 || sp->nattr > BIN_MAX_ATTR) return set_error(BIN_ENOTSUP, "nattr %d not in 0..16", sp->nattr);
     uint64_t B = 1;
