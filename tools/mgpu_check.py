@@ -88,6 +88,49 @@ def main():
             dist.barrier()
         for a in hs:
             db.bin_array_release(a)
+    # fused multi-instance set (bin_multi_*): the paper-step shape (R19) plus an
+    # auto-bounded instance, combined across ranks by the grouped NCCL allreduces
+    n = args.rows // 3
+    r0, r1 = (rank * n) // world, ((rank + 1) * n) // world
+    cols = []
+    for c in range(7):
+        t = torch.empty(r1 - r0, dtype=torch.float64, device=dev)
+        synth.fill_device(synth.UNIFORM, 1, 6, c, r0, r1 - r0, t.data_ptr(), torch.cuda.current_stream(dev).cuda_stream)
+        cols.append(t)
+    torch.cuda.synchronize(dev)
+    hs = [db.wrap_tensor(t) for t in cols]
+    systems = [(0, 1), (0, 2), (1, 2), (4, 5), (4, 6), (5, 6), (0, 4), (1, 5), (2, 6)]
+    insts = [dict(res=(64, 64), lo=(-1.0, -1.0), hi=(1.0, 1.0), axes=sy, attrs=tuple(range(7)), auto=False)
+             for sy in systems] + [dict(res=(50,), axes=(3,), attrs=(4, 5), auto=True)]
+    specs = [db.make_spec(d["res"], None if d["auto"] else d["lo"], None if d["auto"] else d["hi"],
+                          nattr=len(d["attrs"]), bounds_auto=d["auto"]) for d in insts]
+    obj = [db.bin_nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    m = db.bin_multi_init([db.make_multi_op(sp, d["axes"], d["attrs"]) for sp, d in zip(specs, insts)], 7,
+                          db.make_placement(), rank=rank, nranks=world, nccl_id=obj[0])
+    t = db.bin_multi_execute(m, hs)
+    outs = [db.result_to_numpy(m, t, sp, op=k) for k, sp in enumerate(specs)]
+    db.bin_multi_finalize(m)
+    if rank == 0:
+        import oracle
+        host = [synth.fill_host(synth.UNIFORM, 1, 6, c, 0, n) for c in range(7)]
+        for k, (d, out) in enumerate(zip(insts, outs)):
+            ref = oracle.databin([host[i] for i in d["axes"]], [host[i] for i in d["attrs"]], d["res"],
+                                 None if d["auto"] else d["lo"], None if d["auto"] else d["hi"], bounds_auto=d["auto"])
+            status = "ok"
+            try:
+                compare(out, ref)
+                if d["auto"]:
+                    assert np.array_equal(out["lo"], ref["lo"]) and np.array_equal(out["hi"], ref["hi"])
+            except AssertionError as e:  # noqa: PERF203
+                status = "FAIL: " + str(e)[:300]
+                ok = False
+            print(json.dumps({"case": f"multi_instance_{k}", "axes": list(d["axes"]), "world": world, "rows": n,
+                              "res": list(d["res"]), "status": status, "n_in": out["n_in"],
+                              "n_out": out["n_out"]}), flush=True)
+    dist.barrier()
+    for a in hs:
+        db.bin_array_release(a)
     flag = torch.tensor([0 if ok else 1], device=dev)
     dist.broadcast(flag, 0)
     dist.destroy_process_group()
