@@ -50,6 +50,11 @@ def _load():
             lib.oracle_databin.restype = ctypes.c_int
             lib.oracle_bounds.argtypes = [ctypes.c_int, ctypes.c_int64, dpp, d_p, d_p]
             lib.oracle_bounds.restype = ctypes.c_int
+            lib.oracle_exact_sum.argtypes = [ctypes.c_int64, d_p]
+            lib.oracle_exact_sum.restype = ctypes.c_double
+            lib.oracle_exact_sums.argtypes = [ctypes.c_int, i32_p, d_p, d_p, ctypes.c_int64, dpp, ctypes.c_int,
+                                              dpp, d_p]
+            lib.oracle_exact_sums.restype = ctypes.c_int
             lib.oracle_eq1_device.argtypes = [ctypes.c_int] * 5
             lib.oracle_eq1_device.restype = ctypes.c_int
             _lib = lib
@@ -75,12 +80,14 @@ def _as_f64(cols, n=None):
     return out
 
 
-def databin(axes, attrs, res, lo=None, hi=None, bounds_auto=False, P=1):
+def databin(axes, attrs, res, lo=None, hi=None, bounds_auto=False, P=1, exact=False):
     """Bin rows (axes[d][i], attrs[a][i]) onto a res[0] x ... mesh.
 
     Returns a dict with count (u64[B]), sum/sumabs/min/max/avg (f64[A, B]),
     n_in, n_out, lo, hi.  Bins are linearised x fastest (reading R11).
     ``P`` > 1 runs the partition (multi-rank) mode of PAPER.md:479.
+    ``exact``: also ``sum_exact`` / ``avg_exact`` -- each bin's exact sum
+    rounded once (R20; ``oracle_exact_sums``) and it over count.
     """
     lib = _load()
     ndim = len(axes)
@@ -110,9 +117,25 @@ def databin(axes, attrs, res, lo=None, hi=None, bounds_auto=False, P=1):
     if rc != 0:
         raise ValueError(f"oracle_databin failed rc={rc}")
     k = slice(0, nattr)
-    return dict(count=count, sum=s[k], sumabs=sa[k], min=mn[k], max=mx[k], avg=avg[k],
-                n_in=int(n_in.value), n_out=int(n_out.value),
-                lo=loa[:ndim].copy(), hi=hia[:ndim].copy())
+    out = dict(count=count, sum=s[k], sumabs=sa[k], min=mn[k], max=mx[k], avg=avg[k],
+               n_in=int(n_in.value), n_out=int(n_out.value),
+               lo=loa[:ndim].copy(), hi=hia[:ndim].copy())
+    if exact:
+        se = np.zeros(shp, np.float64)
+        rc = lib.oracle_exact_sums(ndim, resa.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), _dptr(loa),
+                                   _dptr(hia), n, _ptr_array(axes), nattr, _ptr_array(attrs), _dptr(se))
+        if rc != 0:
+            raise MemoryError("oracle_exact_sums")
+        out["sum_exact"] = se[k]
+        with np.errstate(invalid="ignore", divide="ignore"):
+            out["avg_exact"] = np.where(count > 0, se[k] / np.maximum(count, 1).astype(np.float64), np.nan)
+    return out
+
+
+def exact_sum(values) -> float:
+    """The exact sum of finite doubles rounded once to nearest-even (R20)."""
+    v = np.ascontiguousarray(values, dtype=np.float64)
+    return float(_load().oracle_exact_sum(v.shape[0], _dptr(v)))
 
 
 def bounds(axes):

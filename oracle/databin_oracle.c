@@ -258,6 +258,150 @@ int oracle_databin(int ndim, const int32_t *res, int bounds_auto,
     return 0;
 }
 
+/* ---- Exact sums (reading R20) ----
+ * The paper's sum reduction over a bin is, as a real number,
+ * the exact sum of the bin's values; its atomic GPU evaluation
+ * rounds in an unspecified order.  The exact-sum mode defines the output as
+ * that exact real sum rounded ONCE to the nearest double (ties to even),
+ * which no summation order changes.  Plain definition: an integer
+ * accumulator in units of 2^-1074 (the spacing of every finite double) wide
+ * enough for any sum of finite doubles, added to exactly, rounded once.
+ * Zero sums are +0.0 (the row-order fold from +0.0 of reading R5 also gives
+ * +0.0 for every zero result).  Precondition: finite values (reading R7). */
+#define XL 36 /* 64-bit limbs, two's complement, bit 0 = 2^-1074 (2304 bits) */
+typedef struct { uint64_t w[XL]; } oracle_xacc;
+
+static void xacc_clear(oracle_xacc *A) { memset(A->w, 0, sizeof A->w); }
+
+/* A += (-1)^s * m * 2^p (units of 2^-1074), m < 2^53, 0 <= p <= 2045 */
+static void xacc_add(oracle_xacc *A, double v)
+{
+    uint64_t bits;
+    memcpy(&bits, &v, 8);
+    int s = (int)(bits >> 63);
+    int e = (int)((bits >> 52) & 0x7ff);
+    uint64_t m = bits & ((1ull << 52) - 1);
+    if (e == 0) e = 1; else m |= 1ull << 52;   /* subnormals share exponent 1 */
+    if (m == 0) return;
+    int p = e - 1;                             /* v = m * 2^(e - 1075) = m * 2^(p - 1074) */
+    int L = p / 64, sh = p % 64;
+    uint64_t part[3] = {m << sh, sh ? (m >> (64 - sh)) : 0, 0};
+    if (!s) {
+        unsigned carry = 0;
+        for (int j = L; j < XL; ++j) {
+            uint64_t add = j - L < 3 ? part[j - L] : 0;
+            uint64_t t = A->w[j] + add;
+            unsigned c1 = t < add;
+            uint64_t t2 = t + carry;
+            unsigned c2 = t2 < t;
+            A->w[j] = t2;
+            carry = c1 | c2;
+            if (j - L >= 2 && !carry) break;
+        }
+    } else {
+        unsigned borrow = 0;
+        for (int j = L; j < XL; ++j) {
+            uint64_t sub = j - L < 3 ? part[j - L] : 0;
+            uint64_t t = A->w[j] - sub;
+            unsigned b1 = A->w[j] < sub;
+            uint64_t t2 = t - borrow;
+            unsigned b2 = t < (uint64_t)borrow;
+            A->w[j] = t2;
+            borrow = b1 | b2;
+            if (j - L >= 2 && !borrow) break;
+        }
+    }
+}
+
+static int xacc_bit(const oracle_xacc *A, int i) { return (int)((A->w[i / 64] >> (i % 64)) & 1u); }
+
+/* The accumulator's exact value rounded once to the nearest double (ties to
+ * even); beyond the largest finite double -> +-inf. */
+static double xacc_round(const oracle_xacc *A0)
+{
+    oracle_xacc A = *A0;
+    int neg = (int)(A.w[XL - 1] >> 63);
+    if (neg) { /* magnitude of a two's complement value: invert and add one */
+        unsigned carry = 1;
+        for (int j = 0; j < XL; ++j) {
+            uint64_t t = ~A.w[j] + carry;
+            carry = carry && t == 0;
+            A.w[j] = t;
+        }
+    }
+    int H = -1; /* highest set bit */
+    for (int i = 64 * XL - 1; i >= 0; --i)
+        if (xacc_bit(&A, i)) { H = i; break; }
+    if (H < 0) return 0.0;
+    uint64_t out;
+    if (H <= 52) {
+        /* fewer than 54 significant bits above 2^-1074: exactly a subnormal, or
+         * the smallest normal binade whose bit pattern is the integer itself */
+        out = A.w[0] & ((1ull << 53) - 1);
+    } else {
+        int shift = H - 52;
+        uint64_t M = 0;
+        for (int i = 52; i >= 0; --i) M = (M << 1) | (uint64_t)xacc_bit(&A, shift + i);
+        int round = xacc_bit(&A, shift - 1), sticky = 0;
+        for (int i = shift - 2; i >= 0 && !sticky; --i) sticky = xacc_bit(&A, i);
+        if (round && (sticky || (M & 1u))) M += 1;
+        if (M == (1ull << 53)) { M >>= 1; shift += 1; }
+        int biased = shift + 1; /* value = M * 2^(shift - 1074), M in [2^52, 2^53) */
+        if (biased >= 2047) out = 0x7ff0000000000000ull;
+        else out = ((uint64_t)biased << 52) | (M & ((1ull << 52) - 1));
+    }
+    if (neg) out |= 1ull << 63;
+    double r;
+    memcpy(&r, &out, 8);
+    return r;
+}
+
+/* Exactly rounded sum of v[0..n). */
+double oracle_exact_sum(int64_t n, const double *v)
+{
+    oracle_xacc A;
+    xacc_clear(&A);
+    for (int64_t i = 0; i < n; ++i) xacc_add(&A, v[i]);
+    return xacc_round(&A);
+}
+
+/* Per-bin exactly rounded sums of every attribute (same binning pass as
+ * oracle_accumulate, bounds already realised): sum[a*nbins + b].
+ * Returns 0, or -2 when the accumulators cannot be allocated. */
+int oracle_exact_sums(int ndim, const int32_t *res, const double *lo, const double *hi,
+                      int64_t n, const double *const *axes, int nattr,
+                      const double *const *attrs, double *sum)
+{
+    int64_t nbins = 1;
+    double scale[ORACLE_MAX_DIM];
+    for (int d = 0; d < ndim; ++d) {
+        nbins *= res[d];
+        scale[d] = (double)res[d] / (hi[d] - lo[d]);
+    }
+    size_t na = (size_t)nattr * (size_t)nbins;
+    oracle_xacc *acc = calloc(na ? na : 1, sizeof(oracle_xacc));
+    if (!acc) return -2;
+    for (int64_t i = 0; i < n; ++i) {
+        int64_t k[ORACLE_MAX_DIM] = {0, 0, 0};
+        int inside = 1;
+        for (int d = 0; d < ndim; ++d) {
+            double x = axes[d][i];
+            if (!(lo[d] <= x && x <= hi[d])) { inside = 0; break; }
+            int64_t kd = (int64_t)floor((x - lo[d]) * scale[d]);
+            if (kd > res[d] - 1) kd = res[d] - 1;
+            k[d] = kd;
+        }
+        if (!inside) continue;
+        int64_t b = k[0];
+        if (ndim >= 2) b += (int64_t)res[0] * k[1];
+        if (ndim >= 3) b += (int64_t)res[0] * res[1] * k[2];
+        for (int a = 0; a < nattr; ++a) xacc_add(&acc[(size_t)a * nbins + b], attrs[a][i]);
+    }
+    for (size_t j = 0; j < na; ++j) sum[j] = xacc_round(&acc[j]);
+    free(acc);
+    return 0;
+}
+
 /* ---- Automatic device selection, Eq. (1) ----
  *   d = ( r mod n_u * s + d_0 ) mod n_a
  * read (reading R14) as ((r mod n_u) * s + d_0) mod n_a, which is also the
