@@ -49,6 +49,7 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=10.0)
     p.add_argument("--bounds-auto", action="store_true")
     p.add_argument("--deterministic", action="store_true")
+    p.add_argument("--exact", action="store_true", help="BIN_SUM_EXACT: correctly rounded exact sums (R20)")
     return p.parse_args()
 
 
@@ -234,7 +235,7 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
     spec = db.make_spec(w.res, w.lo, w.hi, nattr=len(w.attrs), ops=w.ops, bounds_auto=args.bounds_auto,
-                        deterministic=args.deterministic)
+                        deterministic=args.deterministic, exact=args.exact)
     place = db.make_placement(device_id=db.BIN_DEVICE_AUTO)  # Eq. (1): rank -> device
     h = db.bin_init(spec, place, rank=rank, nranks=world, nccl_id=nccl_id)
     arrs = [db.wrap_tensor(cols[c], stream=stream.cuda_stream, mode=db.BIN_ASYNC) for c in list(w.axes) + list(w.attrs)]
@@ -343,6 +344,7 @@ def main():
                        "bounds": "auto" if args.bounds_auto else [list(w.lo), list(w.hi)],
                        "axes": list(w.axes), "attrs": list(w.attrs), "ops": list(w.ops),
                        "exec": "lockstep (BIN_EXEC_SYNC, stream-ordered)", "deterministic": args.deterministic,
+                       "sum_mode": "exact (BIN_SUM_EXACT)" if args.exact else "fast",
                        "l2": "inputs 24 B/row x rows >> 126 MB L2; no flush needed",
                        "parallelism": f"dp{world} (contiguous row shards per rank)", "combine": combine},
             "hbm": {"alg_bytes_per_step": step_alg_bytes,

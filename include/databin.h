@@ -162,8 +162,17 @@ typedef struct {
                                    deterministic; falls back to the window route when the
                                    partition plan does not apply (> 4 attributes read, n >= 2^32,
                                    unaligned columns, > 8192 tiles). */
+    int32_t sum_mode;           /* BIN_SUM_FAST (0, default): sums accumulated in an unspecified order
+                                   (within 1e-12 * sum|v| of the row-order sum, R8);
+                                   BIN_SUM_EXACT: every bin's sum is its exact real sum rounded once
+                                   to nearest-even (R20; zero -> +0.0, beyond DBL_MAX ->
+                                   +-inf), avg = that sum / count -- identical across runs, routes and
+                                   rank counts.  Needs finite attribute values (R7), fewer than 2^30
+                                   rows per execute and rank, and deterministic == 0 (else BIN_EINVAL);
+                                   costs 66 x 8 bytes per bin and summed attribute of device memory. */
 } bin_spec_t;
 enum { BIN_ROUTE_AUTO = 0, BIN_ROUTE_WINDOW = 1, BIN_ROUTE_PARTITION = 2 };
+enum { BIN_SUM_FAST = 0, BIN_SUM_EXACT = 1 };
 
 /* Execution method + placement (Sec. 3; XML attributes at PAPER.md:426-433). */
 enum { BIN_EXEC_SYNC = 0, BIN_EXEC_ASYNC = 1, BIN_EXEC_PEER = 2 };

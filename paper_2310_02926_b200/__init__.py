@@ -18,7 +18,7 @@ from .capi import (  # noqa: F401
     BIN_ALLOC_CUDA, BIN_ALLOC_CUDA_ASYNC, BIN_ALLOC_CUDA_UVA, BIN_ALLOC_EXTERNAL, BIN_ALLOC_HOST,
     BIN_ALLOC_HOST_PINNED, BIN_ASYNC, BIN_DEVICE_AUTO, BIN_DEVICE_HOST, BIN_EXEC_ASYNC, BIN_EXEC_PEER,
     BIN_EXEC_SYNC, BIN_F64, BIN_OP_AVG, BIN_OP_MAX, BIN_OP_MIN, BIN_OP_SUM, BIN_ROUTE_AUTO, BIN_ROUTE_PARTITION,
-    BIN_ROUTE_WINDOW, BIN_SYNC, EXPORTED, OPS, ROUTES,
+    BIN_ROUTE_WINDOW, BIN_SUM_EXACT, BIN_SUM_FAST, BIN_SYNC, EXPORTED, OPS, ROUTES,
     BIN_MULTI_MAX_COLS, BIN_MULTI_MAX_OPS, RELEASE_FN, BinError, bin_comm_t, bin_multi_op_t, bin_placement_t, bin_profile_t, bin_result_t, bin_spec_t, check, lib)
 
 _lib = lib()  # load (and build if stale) at import: no silent fallback
@@ -81,7 +81,7 @@ def bin_alloc_stats():
 
 # ---------------------------------------------------------------- operator
 def make_spec(res, lo=None, hi=None, nattr=0, ops=("sum", "min", "max", "avg"), bounds_auto=False,
-              deterministic=False, route="auto") -> bin_spec_t:
+              deterministic=False, route="auto", exact=False) -> bin_spec_t:
     """Builds a bin_spec_t; ``ops`` is one op tuple for all attributes or a list per attribute."""
     s = bin_spec_t()
     s.ndim = len(res)
@@ -101,6 +101,7 @@ def make_spec(res, lo=None, hi=None, nattr=0, ops=("sum", "min", "max", "avg"), 
         s.ops[a] = m
     s.deterministic = int(bool(deterministic))
     s.route = ROUTES[route] if isinstance(route, str) else int(route)
+    s.sum_mode = BIN_SUM_EXACT if exact else BIN_SUM_FAST
     return s
 
 

@@ -29,6 +29,7 @@ BIN_EXEC_SYNC, BIN_EXEC_ASYNC, BIN_EXEC_PEER = 0, 1, 2
 BIN_DEVICE_HOST, BIN_DEVICE_AUTO = -1, -2
 BIN_ROUTE_AUTO, BIN_ROUTE_WINDOW, BIN_ROUTE_PARTITION = 0, 1, 2
 ROUTES = {"auto": BIN_ROUTE_AUTO, "window": BIN_ROUTE_WINDOW, "partition": BIN_ROUTE_PARTITION}
+BIN_SUM_FAST, BIN_SUM_EXACT = 0, 1
 
 
 class BinError(RuntimeError):
@@ -41,7 +42,8 @@ class BinError(RuntimeError):
 class bin_spec_t(ctypes.Structure):
     _fields_ = [("ndim", ctypes.c_int32), ("res", ctypes.c_int32 * 3), ("bounds_auto", ctypes.c_int32),
                 ("lo", ctypes.c_double * 3), ("hi", ctypes.c_double * 3), ("nattr", ctypes.c_int32),
-                ("ops", ctypes.c_uint32 * 16), ("deterministic", ctypes.c_int32), ("route", ctypes.c_int32)]
+                ("ops", ctypes.c_uint32 * 16), ("deterministic", ctypes.c_int32), ("route", ctypes.c_int32),
+                ("sum_mode", ctypes.c_int32)]
 
 
 class bin_placement_t(ctypes.Structure):

@@ -17,6 +17,7 @@
 
 #include "db_internal.h"
 #include "dev_common.cuh"
+#include "xsum.cuh"
 
 namespace db {
 
@@ -115,14 +116,24 @@ __device__ __forceinline__ uint32_t fast_row(const FastCtx<D> &c, const double (
 // global rows' min/max first read the slot pair from L2 and reduce only when
 // they improve it (stale reads are safe: the slots only decrease), which turns
 // two L2 atomics per global row into one load for all but the first rows.
-template <int A, int SM, int MM>
+// Exact sums (BIN_SUM_EXACT): digit rows instead of the f64 reduction.
+struct FastX {
+    long long *xs;  // nullptr: BIN_SUM_FAST
+    uint64_t B;
+    int *sxr;       // this CTA's touched digit range (shared memory)
+};
+
+template <int A, int SM, int MM, bool XS>
 __device__ __forceinline__ void fast_exec(uint32_t tag, double v, unsigned long long *count, double *sum,
-                                          ulonglong2 *mm, bool gf) {
+                                          ulonglong2 *mm, bool gf, const FastX &X) {
     constexpr bool HS = A == 1 && SM == 1, HM = A == 1 && MM == 1;
     const uint32_t kind = tag >> 29, b = tag & QBIN;
     if (kind & QK_GLOBAL) {
         if (!(kind & QK_MIN)) atomicAdd(&count[b], 1ull);  // QK_GLOBAL|QK_MIN marks "count already counted"
-        if (HS) atomicAdd(&sum[b], v);
+        if (HS) {
+            if (XS) xsum_add_double(X.xs, X.B, 0, b, v, X.sxr);
+            else atomicAdd(&sum[b], v);
+        }
         if (HM) {
             const unsigned long long e = enc_total(v);
             ulonglong2 cur = make_ulonglong2(~0ull, ~0ull);
@@ -137,9 +148,10 @@ __device__ __forceinline__ void fast_exec(uint32_t tag, double v, unsigned long 
     }
 }
 
-template <int A, int SM, int MM>
+template <int A, int SM, int MM, bool XS>
 __device__ __forceinline__ void fast_push(uint32_t qb, uint32_t &qn, uint32_t tag, double v, unsigned lane,
-                                          unsigned long long *count, double *sum, ulonglong2 *mm, bool gf) {
+                                          unsigned long long *count, double *sum, ulonglong2 *mm, bool gf,
+                                          const FastX &X) {
     const unsigned m = __ballot_sync(0xffffffffu, tag != 0);
     if (m == 0) return;
     double *vals = (double *)&f_dsm[qb + QCAP];
@@ -166,7 +178,7 @@ __device__ __forceinline__ void fast_push(uint32_t qb, uint32_t &qn, uint32_t ta
             vals[lane] = v2;
         }
         qn = rest;
-        fast_exec<A, SM, MM>(t, vv, count, sum, mm, gf);
+        fast_exec<A, SM, MM, XS>(t, vv, count, sum, mm, gf, X);
         __syncwarp();
     }
 }
@@ -238,7 +250,7 @@ __device__ __forceinline__ void fast_choose_window(const DGeom G, const WinPlan 
     __syncthreads();  // the histogram scratch becomes the window after this
 }
 
-template <int D, int A, int SM, int MM>
+template <int D, int A, int SM, int MM, bool XS>
 __global__ void __launch_bounds__(FAST_THREADS, 1)
     k_bin_fast(Geom g, Inputs in, Accum acc, uint32_t npairs, int head, int wcap, int32_t *wcache, int reuse,
                unsigned long long *ktrace) {
@@ -254,6 +266,8 @@ __global__ void __launch_bounds__(FAST_THREADS, 1)
     __shared__ unsigned long long s_best[FAST_THREADS / 32];
     __shared__ int s_origin[6];
     __shared__ unsigned s_exp;
+    __shared__ int s_xr[2 * BIN_MAX_ATTR];
+    if (XS) xr_init(s_xr);
     FastCtx<D> c;
     unsigned long long *const count = acc.count;
     double *const sum = acc.sum;
@@ -325,6 +339,7 @@ __global__ void __launch_bounds__(FAST_THREADS, 1)
     for (uint32_t i = c.o_fx + threadIdx.x; i < o_end; i += FAST_THREADS) f_dsm[i] = 0u;
     const unsigned lane = threadIdx.x & 31u;
     const uint32_t qb = ((o_end + 3u) & ~3u) + (threadIdx.x >> 5) * QWORDS;
+    const FastX X{XS ? acc.xs : nullptr, acc.nbins, s_xr};
     uint32_t qn = 0;
     __syncthreads();
 
@@ -344,11 +359,11 @@ __global__ void __launch_bounds__(FAST_THREADS, 1)
 #pragma unroll
         for (int d = 0; d < D; ++d) x[d] = bx[d].x;
         uint32_t t0 = fast_row<D, A, SM, MM>(c, x, bv.x, valid, n_in);
-        fast_push<A, SM, MM>(qb, qn, t0, bv.x, lane, count, sum, mm, gf);
+        fast_push<A, SM, MM, XS>(qb, qn, t0, bv.x, lane, count, sum, mm, gf, X);
 #pragma unroll
         for (int d = 0; d < D; ++d) x[d] = bx[d].y;
         uint32_t t1 = fast_row<D, A, SM, MM>(c, x, bv.y, valid, n_in);
-        fast_push<A, SM, MM>(qb, qn, t1, bv.y, lane, count, sum, mm, gf);
+        fast_push<A, SM, MM, XS>(qb, qn, t1, bv.y, lane, count, sum, mm, gf, X);
         rows += valid ? 2u : 0u;
 #pragma unroll
         for (int d = 0; d < D; ++d) bx[d] = nx[d];
@@ -364,10 +379,10 @@ __global__ void __launch_bounds__(FAST_THREADS, 1)
         if (A == 1 && r >= 0) v = in.at[0][r];
         const uint32_t t = fast_row<D, A, SM, MM>(c, x, v, r >= 0, n_in);
         rows += r >= 0 ? 1u : 0u;
-        fast_push<A, SM, MM>(qb, qn, t, v, lane, count, sum, mm, gf);
+        fast_push<A, SM, MM, XS>(qb, qn, t, v, lane, count, sum, mm, gf, X);
     }
     __syncwarp();
-    if (lane < qn) fast_exec<A, SM, MM>(f_dsm[qb + lane], ((double *)&f_dsm[qb + QCAP])[lane], count, sum, mm, gf);
+    if (lane < qn) fast_exec<A, SM, MM, XS>(f_dsm[qb + lane], ((double *)&f_dsm[qb + QCAP])[lane], count, sum, mm, gf, X);
 
     unsigned long long in_w = n_in, out_w = rows - n_in;
 #pragma unroll
@@ -397,9 +412,18 @@ __global__ void __launch_bounds__(FAST_THREADS, 1)
         atomicAdd(&count[b], cnt);
         if (HS) {
             const uint32_t w0 = c.o_fx + l;
-            const double d = fx_to_double(f_dsm[w0], f_dsm[w0 + W], f_dsm[w0 + 2 * W], cnt, c.fx.inv_scale);
-            if (d != 0.0) atomicAdd(&sum[b], d);
+            if (XS) {
+                xsum_add_fixed(X.xs, X.B, 0, b, f_dsm[w0], f_dsm[w0 + W], f_dsm[w0 + 2 * W], cnt, FX_OFFSET, c.fx.F,
+                               s_xr);
+            } else {
+                const double d = fx_to_double(f_dsm[w0], f_dsm[w0 + W], f_dsm[w0 + 2 * W], cnt, c.fx.inv_scale);
+                if (d != 0.0) atomicAdd(&sum[b], d);
+            }
         }
+    }
+    if (XS) {
+        __syncthreads();
+        xr_publish(s_xr, 1, acc.xrange);
     }
     if (ktrace) {
         __syncthreads();
@@ -420,7 +444,7 @@ bool fast_eligible(const Inputs &in, const Accum &acc, int ndim) {
     return in.n >= 2 + head && (in.n - head) / 2 < (1ll << 31);
 }
 
-template <int D, int A, int SM, int MM>
+template <int D, int A, int SM, int MM, bool XS>
 static cudaError_t launch_fast_t(const Geom &g, const Inputs &in, const Accum &acc, const LaunchCfg &lc, int smem,
                                  int wcap, int32_t *wcache, int reuse, unsigned long long *ktrace, cudaStream_t s) {
     const int head = ((uintptr_t)in.ax[0] & 15u) ? 1 : 0;
@@ -428,7 +452,7 @@ static cudaError_t launch_fast_t(const Geom &g, const Inputs &in, const Accum &a
     int blocks = lc.sms;  // one persistent CTA per SM: the whole shared memory holds the window
     const int64_t maxb = ((int64_t)npairs + FAST_THREADS - 1) / FAST_THREADS;
     if (maxb < blocks) blocks = (int)(maxb > 0 ? maxb : 1);
-    auto kern = k_bin_fast<D, A, SM, MM>;
+    auto kern = k_bin_fast<D, A, SM, MM, XS>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     kern<<<blocks, FAST_THREADS, smem, s>>>(g, in, acc, npairs, head, wcap, wcache, reuse, ktrace);
@@ -439,11 +463,17 @@ template <int D>
 static cudaError_t launch_fast_d(const Geom &g, const Inputs &in, const Accum &acc, const LaunchCfg &lc, int smem,
                                  int wcap, int32_t *wc, int reuse, unsigned long long *kt, cudaStream_t s) {
     if (in.nattr == 0 || !(acc.load_mask & 1u))
-        return launch_fast_t<D, 0, 0, 0>(g, in, acc, lc, smem, wcap, wc, reuse, kt, s);
-    const bool sm = acc.sum_mask & 1u, mm = acc.mm_mask & 1u;
-    if (sm && mm) return launch_fast_t<D, 1, 1, 1>(g, in, acc, lc, smem, wcap, wc, reuse, kt, s);
-    if (sm) return launch_fast_t<D, 1, 1, 0>(g, in, acc, lc, smem, wcap, wc, reuse, kt, s);
-    return launch_fast_t<D, 1, 0, 1>(g, in, acc, lc, smem, wcap, wc, reuse, kt, s);
+        return launch_fast_t<D, 0, 0, 0, false>(g, in, acc, lc, smem, wcap, wc, reuse, kt, s);
+    const bool sm = acc.sum_mask & 1u, mm = acc.mm_mask & 1u, xs = acc.xs != nullptr;
+    if (sm && mm) {
+        if (xs) return launch_fast_t<D, 1, 1, 1, true>(g, in, acc, lc, smem, wcap, wc, reuse, kt, s);
+        return launch_fast_t<D, 1, 1, 1, false>(g, in, acc, lc, smem, wcap, wc, reuse, kt, s);
+    }
+    if (sm) {
+        if (xs) return launch_fast_t<D, 1, 1, 0, true>(g, in, acc, lc, smem, wcap, wc, reuse, kt, s);
+        return launch_fast_t<D, 1, 1, 0, false>(g, in, acc, lc, smem, wcap, wc, reuse, kt, s);
+    }
+    return launch_fast_t<D, 1, 0, 1, false>(g, in, acc, lc, smem, wcap, wc, reuse, kt, s);
 }
 
 cudaError_t launch_bin_fast(const Geom &g, const Inputs &in, const Accum &acc, const LaunchCfg &lc, int smem,

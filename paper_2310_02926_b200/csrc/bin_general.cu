@@ -10,7 +10,7 @@
 // On sm_100a the only native shared-memory atomics are 32-bit integer ones
 // (ATOMS.ADD/MIN); f32/f64/u64 adds and u64 min are ATOMS.CAST.SPIN CAS loops
 // (~2 L1 wavefronts per lane; profiles/r01_kbin_ncu_v1_cas.txt).  Hence:
-//  * sums: exact 96-bit integer of q' = round(v*2^F) + 2^54 with native u32
+//  * sums: exact 96-bit integer of q' = round(v*2^F) + 2^62 with native u32
 //    atomics and carry propagation from the returned old value
 //      old = atomicAdd(lo, q'_lo); carry = (old + q'_lo wrapped)
 //      old = atomicAdd(mid, q'_mid + carry); if wrapped: atomicAdd(hi, 1)
@@ -26,6 +26,7 @@
 
 #include "db_internal.h"
 #include "dev_common.cuh"
+#include "xsum.cuh"
 
 namespace db {
 
@@ -42,6 +43,8 @@ struct GenCtx {
     ulonglong2 *mm;
     uint64_t nbins;
     uint32_t sum_mask, mm_mask;
+    long long *xs;  // BIN_SUM_EXACT digit rows (xsum.cuh), nullptr for BIN_SUM_FAST
+    int *sxr;       // this CTA's touched digit ranges (shared memory)
 };
 
 template <int D>
@@ -89,7 +92,8 @@ __device__ __forceinline__ void accumulate_row(const GenCtx &c, const FxParam (&
                     const unsigned old = atomicAdd(&g_dsm[w0], qlo);
                     qmid += (old + qlo < old) ? 1u : 0u;
                 } else {  // rare: outside the fixed range -> f64 L2 reduction, offset only here
-                    atomicAdd(&c.sum[(uint64_t)s * c.nbins + global_bin<D>(c, k)], v[a]);
+                    if (c.xs) xsum_add_double(c.xs, c.nbins, (int)s, global_bin<D>(c, k), v[a], c.sxr);
+                    else atomicAdd(&c.sum[(uint64_t)s * c.nbins + global_bin<D>(c, k)], v[a]);
                     qmid = FX_OFFSET_MID;
                 }
                 const unsigned old2 = atomicAdd(&g_dsm[w0 + W], qmid);
@@ -120,8 +124,11 @@ __device__ __forceinline__ void accumulate_row(const GenCtx &c, const FxParam (&
         atomicAdd(&c.count[b], 1ull);
 #pragma unroll
         for (int a = 0; a < A; ++a) {
-            if ((c.sum_mask >> a) & 1u)
-                atomicAdd(&c.sum[(uint64_t)__popc(c.sum_mask & ((1u << a) - 1u)) * c.nbins + b], v[a]);
+            if ((c.sum_mask >> a) & 1u) {
+                const uint32_t s = __popc(c.sum_mask & ((1u << a) - 1u));
+                if (c.xs) xsum_add_double(c.xs, c.nbins, (int)s, b, v[a], c.sxr);
+                else atomicAdd(&c.sum[(uint64_t)s * c.nbins + b], v[a]);
+            }
             if ((c.mm_mask >> a) & 1u) {
                 ulonglong2 *p = &c.mm[(uint64_t)__popc(c.mm_mask & ((1u << a) - 1u)) * c.nbins + b];
                 const unsigned long long e = enc_total(v[a]);
@@ -138,7 +145,11 @@ struct GenThreads { static constexpr int value = A <= 1 ? 1024 : 512; };
 template <int D, int A, bool VEC>
 __global__ void __launch_bounds__(GenThreads<A>::value, 1)
     k_bin(Geom g, Inputs in, Accum acc, int64_t head) {
+    __shared__ int s_xr[2 * BIN_MAX_ATTR];
+    xr_init(s_xr);
     GenCtx c;
+    c.xs = acc.xs;
+    c.sxr = s_xr;
     c.G = load_geom<D>(g, acc.bounds);
     if (!c.G.ok) return;  // degenerate auto bounds: finalize reports it
     c.w = load_window(c.G, acc.window, D);
@@ -244,10 +255,19 @@ __global__ void __launch_bounds__(GenThreads<A>::value, 1)
             if ((c.sum_mask >> a) & 1u) {
                 const uint32_t s = __popc(c.sum_mask & ((1u << a) - 1u));
                 const uint32_t w0 = c.o_fx + s * 3 * W + l;
-                const double d = fx_to_double(g_dsm[w0], g_dsm[w0 + W], g_dsm[w0 + 2 * W], cnt, fx[a].inv_scale);
-                if (d != 0.0) atomicAdd(&c.sum[(uint64_t)s * c.nbins + b], d);
+                if (c.xs) {
+                    xsum_add_fixed(c.xs, c.nbins, (int)s, b, g_dsm[w0], g_dsm[w0 + W], g_dsm[w0 + 2 * W], cnt,
+                                   FX_OFFSET, fx[a].F, s_xr);
+                } else {
+                    const double d = fx_to_double(g_dsm[w0], g_dsm[w0 + W], g_dsm[w0 + 2 * W], cnt, fx[a].inv_scale);
+                    if (d != 0.0) atomicAdd(&c.sum[(uint64_t)s * c.nbins + b], d);
+                }
             }
         }
+    }
+    if (c.xs) {
+        __syncthreads();
+        xr_publish(s_xr, acc.nsum, acc.xrange);
     }
 }
 

@@ -34,6 +34,7 @@
 
 #include "db_internal.h"
 #include "dev_common.cuh"
+#include "xsum.cuh"
 
 namespace db {
 
@@ -520,6 +521,8 @@ __global__ void __launch_bounds__(PART_THREADS, 1) k_part_reduce(Accum acc, Part
     const uint32_t lo = (uint32_t)(((uint64_t)ns * blockIdx.x) / gridDim.x);
     const uint32_t hi = (uint32_t)(((uint64_t)ns * (blockIdx.x + 1)) / gridDim.x);
     if (lo >= hi) return;
+    __shared__ int s_xr[2 * BIN_MAX_ATTR];  // BIN_SUM_EXACT: digits this CTA touched (xsum.cuh)
+    xr_init(s_xr);
     const int nl = pa.nl;
     const uint32_t sum_mask = acc.sum_mask, mm_mask = acc.mm_mask;
     int ss[AA], ms[AA];  // sum / min-max slot of load slot j, -1 if none
@@ -634,7 +637,8 @@ __global__ void __launch_bounds__(PART_THREADS, 1) k_part_reduce(Accum acc, Part
                             const unsigned old = atomicAdd(&p_dsm[w0], qlo);
                             qmid += (old + qlo < old) ? 1u : 0u;
                         } else {  // outside the fixed range: f64 L2 reduction, offset only here
-                            atomicAdd(&acc.sum[(uint64_t)ss[j] * B + base + l], x);
+                            if (acc.xs) xsum_add_double(acc.xs, B, ss[j], base + l, x, s_xr);
+                            else atomicAdd(&acc.sum[(uint64_t)ss[j] * B + base + l], x);
                             qmid = FX_OFFSET_MID;
                         }
                         const unsigned old2 = atomicAdd(&p_dsm[w0 + W], qmid);
@@ -660,8 +664,14 @@ __global__ void __launch_bounds__(PART_THREADS, 1) k_part_reduce(Accum acc, Part
             for (int j = 0; j < A; ++j) {
                 if (ss[j] >= 0) {
                     const uint32_t w0 = o_fx + (uint32_t)ss[j] * 3u * W + l;
-                    const double d = fx_to_double(p_dsm[w0], p_dsm[w0 + W], p_dsm[w0 + 2 * W], cnt, fx[j].inv_scale);
-                    if (d != 0.0) atomicAdd(&acc.sum[(uint64_t)ss[j] * B + b], d);
+                    if (acc.xs) {
+                        xsum_add_fixed(acc.xs, B, ss[j], b, p_dsm[w0], p_dsm[w0 + W], p_dsm[w0 + 2 * W], cnt,
+                                       FX_OFFSET, fx[j].F, s_xr);
+                    } else {
+                        const double d =
+                            fx_to_double(p_dsm[w0], p_dsm[w0 + W], p_dsm[w0 + 2 * W], cnt, fx[j].inv_scale);
+                        if (d != 0.0) atomicAdd(&acc.sum[(uint64_t)ss[j] * B + b], d);
+                    }
                 }
                 if (ms[j] >= 0) {
                     const ulonglong2 m = wmm[(uint32_t)ms[j] * W + l];
@@ -673,6 +683,7 @@ __global__ void __launch_bounds__(PART_THREADS, 1) k_part_reduce(Accum acc, Part
         }
         __syncthreads();
     }
+    if (acc.xs) xr_publish(s_xr, acc.nsum, acc.xrange);  // (after the last tile's barrier)
 }
 
 // ---------------------------------------------------------------- host side

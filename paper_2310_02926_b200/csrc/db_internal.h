@@ -75,6 +75,8 @@ bool is_device_memory(const bin_array *a);
 // ---------------------------------------------------------------- kernels
 namespace db {
 
+constexpr int XD_DIGITS = 66;  // exact-sum digits per (summed attribute, bin): xsum.cuh XD
+
 struct Geom {
     int32_t ndim;
     int32_t res[3];
@@ -102,6 +104,9 @@ struct Accum {
     int32_t *window;            // 6 ints: origin[3], extent[3]
     uint32_t *fxexp;            // 16: max biased exponent of each summed attribute over the sample
     double *omin, *omax, *oavg; // outputs
+    long long *xs;              // BIN_SUM_EXACT: nsum x XD x nbins carry-save digits (xsum.cuh), else nullptr
+    int32_t *xrange;            // BIN_SUM_EXACT: 2 * nsum {min digit, -max digit} touched by the slot's
+                                // last execute (init zeroes them, then resets the range)
     uint64_t nbins;
     int32_t nsum, nmm;
     uint32_t sum_mask, mm_mask, load_mask;

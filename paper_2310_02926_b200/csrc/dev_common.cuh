@@ -90,14 +90,15 @@ __device__ __forceinline__ bool bin_coords(const DGeom &G, const double (&x)[D],
 }
 
 // ---- fixed-point window sums (see bin_general.cu / bin_fast.cu headers) ----
-// q' = round(v * 2^F) + 2^54 with |round(v * 2^F)| < 2^54, summed exactly in
-// 96 bits; the flush subtracts count * 2^54.  (The count cannot be recovered
-// from the sum alone: sum q / 2^55 is not bounded by 1/2 -- tried and
+// q' = round(v * 2^F) + 2^62 with |round(v * 2^F)| < 2^62, summed exactly in
+// 96 bits; the flush subtracts count * 2^62.  (The count cannot be recovered
+// from the sum alone: sum q / 2^63 is not bounded by 1/2 -- tried and
 // rejected, WE4 catches it -- so windows keep an explicit count.)
-constexpr long long FX_OFFSET = 1ll << 54;
+constexpr long long FX_OFFSET = 1ll << 62;
 constexpr unsigned FX_OFFSET_MID = (unsigned)(FX_OFFSET >> 32);
 
 struct FxParam {
+    int F;
     double scale;      // 2^F
     double inv_scale;  // 2^-F
     unsigned lo;       // biased exponents [lo, lo + span) take the fixed path (plus exact 0)
@@ -105,14 +106,17 @@ struct FxParam {
 };
 
 // F from the sampled max exponent of the attribute: E_hi = e_max + 3 (biased
-// eb_hi), F = 54 - E_hi; values in [2^(E_hi-9), 2^E_hi) -> quantisation <= 2^-46 |v|.
+// eb_hi), F = 62 - E_hi; values in [2^(E_hi-9), 2^E_hi) have their last
+// mantissa bit at or above 2^(E_hi-61) >= 2^-F, so round(v * 2^F) is exact:
+// the window sums are exact integers (|q| < 2^62, 96 bits hold 2^33 of them).
 __device__ __forceinline__ FxParam fx_param(unsigned fxexp) {
     int eb_hi = (int)fxexp + 3;
     if (fxexp == 0) eb_hi = 1023 + 1;  // nothing sampled: assume |v| < 2
-    const int F = 54 - (eb_hi - 1023);
+    const int F = 62 - (eb_hi - 1023);
     const bool usable = F > -900 && F < 900;
     const int eb_lo = max(eb_hi - 9, 1);
     FxParam P;
+    P.F = F;
     P.lo = usable ? (unsigned)eb_lo : 1u;
     P.span = usable ? (unsigned)(eb_hi - eb_lo) : 0u;
     P.scale = usable ? ldexp(1.0, F) : 0.0;
@@ -125,7 +129,7 @@ __device__ __forceinline__ bool fx_path(const FxParam &P, double v) {
     return eb - P.lo < P.span || v == 0.0;
 }
 
-// q' = round(v * 2^F) + 2^54 in (0, 2^55)
+// q' = round(v * 2^F) + 2^62 in (0, 2^63)
 __device__ __forceinline__ unsigned long long fx_quant(const FxParam &P, double v) {
     return (unsigned long long)(__double2ll_rn(__dmul_rn(v, P.scale)) + FX_OFFSET);
 }

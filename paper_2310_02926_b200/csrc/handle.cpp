@@ -185,7 +185,10 @@ static int alloc_slot(bin_handle *h, Slot &s) {
     size_t o_omax = o_omin + al(B * 8 * h->nmm);
     size_t o_oavg = o_omax + al(B * 8 * h->nmm);
     size_t o_meta = o_oavg + al(B * 8 * h->nsum);
-    size_t total = o_meta + al(sizeof(Meta));
+    const bool exact = h->spec.sum_mode == BIN_SUM_EXACT && h->nsum > 0;
+    size_t o_xrange = o_meta + al(sizeof(Meta));
+    size_t o_xs = o_xrange + al(2 * BIN_MAX_ATTR * 4);
+    size_t total = exact ? o_xs + al(B * 8 * XD_DIGITS * h->nsum) : o_xrange;
     unsigned char *base = nullptr;
     cudaError_t e = cudaMalloc(&base, total);
     s.base = base;
@@ -205,6 +208,12 @@ static int alloc_slot(bin_handle *h, Slot &s) {
     s.acc.omin = (double *)(base + o_omin);
     s.acc.omax = (double *)(base + o_omax);
     s.acc.oavg = (double *)(base + o_oavg);
+    if (exact) {
+        s.acc.xrange = (int32_t *)(base + o_xrange);
+        s.acc.xs = (long long *)(base + o_xs);
+        if ((e = cudaMemset(s.acc.xrange, 0x7f, 2 * BIN_MAX_ATTR * 4)) != cudaSuccess)
+            return cuda_error(e, "bin_init memset(xrange)");
+    }
     s.acc.nbins = B;
     s.acc.nsum = h->nsum;
     s.acc.nmm = h->nmm;
@@ -239,6 +248,10 @@ int db::validate_spec(const bin_spec_t *sp, uint64_t *nbins) {
                 return set_error(BIN_EINVAL, "axis %d: hi - lo overflows", d);
         }
     }
+    if (sp->sum_mode != BIN_SUM_FAST && sp->sum_mode != BIN_SUM_EXACT)
+        return set_error(BIN_EINVAL, "sum_mode %d is not a BIN_SUM_* value", sp->sum_mode);
+    if (sp->sum_mode == BIN_SUM_EXACT && sp->deterministic)
+        return set_error(BIN_EINVAL, "BIN_SUM_EXACT and deterministic are exclusive (exact sums are order-free)");
     if (sp->route < BIN_ROUTE_AUTO || sp->route > BIN_ROUTE_PARTITION)
         return set_error(BIN_EINVAL, "route %d is not a BIN_ROUTE_* value", sp->route);
     for (int a = 0; a < sp->nattr; ++a)
@@ -498,7 +511,7 @@ int bin_init(const bin_spec_t *spec, const bin_placement_t *place, const bin_com
             h->comm = nullptr;
             return fail(nccl_error(r, "ncclCommInitRank"));
         }
-        h->peer = setup_peer(h);
+        h->peer = h->spec.sum_mode != BIN_SUM_EXACT && setup_peer(h);  // exact: digits go through NCCL
     }
     *out = h;
     return BIN_OK;
@@ -669,6 +682,8 @@ int bin_execute(bin_handle_t *h, bin_array_t *const *axes, int32_t naxes, bin_ar
     };
     int rc;
     if ((rc = rec(EV_INIT0, staged_any))) return rc;
+    if (S.acc.xs && n >= (1ll << 30))
+        return set_error(BIN_EINVAL, "BIN_SUM_EXACT: %lld rows per execute (limit 2^30: digit headroom)", (long long)n);
     // ---- route: partition (bin_part.cu) or window; auto follows the last probe
     PartArgs pa{};
     const bool part_ok = n > 0 && !h->spec.deterministic && h->spec.route != BIN_ROUTE_WINDOW &&
@@ -703,6 +718,8 @@ int bin_execute(bin_handle_t *h, bin_array_t *const *axes, int32_t naxes, bin_ar
     if ((e = launch_init(geom, in, S.acc, h->wcap, false, h->prep)) != cudaSuccess)
         return cuda_error(e, "init kernel");
     S.launches++;
+    if (S.acc.xs)  // exact sums: the digits of the last execute are clear; reset their range
+        DB_CUDA(cudaMemsetAsync(S.acc.xrange, 0x7f, 2 * BIN_MAX_ATTR * 4, h->prep));
     DB_CUDA(cudaEventRecord(S.zeroed, h->prep));
     DB_CUDA(cudaStreamWaitEvent(s, S.zeroed, 0));
     const bool window_in_prep = !geom.bounds_auto && !h->spec.deterministic && !fast && !part;
@@ -788,8 +805,13 @@ int bin_execute(bin_handle_t *h, bin_array_t *const *axes, int32_t naxes, bin_ar
         const uint64_t B = h->nbins;
         ncclResult_t r = ncclGroupStart();
         if (r == ncclSuccess) r = ncclAllReduce(S.acc.count, S.acc.count, B + 2, ncclUint64, ncclSum, h->comm, s);
-        if (r == ncclSuccess && h->nsum && !h->gather)
+        if (r == ncclSuccess && h->nsum && !h->gather && !S.acc.xs)
             r = ncclAllReduce(S.acc.sum, S.acc.sum, B * h->nsum, ncclFloat64, ncclSum, h->comm, s);
+        if (r == ncclSuccess && S.acc.xs) {  // exact sums: digits add as integers (order-free), ranges unite
+            r = ncclAllReduce(S.acc.xs, S.acc.xs, B * h->nsum * XD_DIGITS, ncclInt64, ncclSum, h->comm, s);
+            if (r == ncclSuccess)
+                r = ncclAllReduce(S.acc.xrange, S.acc.xrange, 2 * h->nsum, ncclInt32, ncclMin, h->comm, s);
+        }
         if (r == ncclSuccess && h->nsum && h->gather)  // deterministic: gather partials, fold in rank order
             r = ncclAllGather(S.acc.sum, h->gather, B * h->nsum, ncclFloat64, h->comm, s);
         if (r == ncclSuccess && h->nmm)

@@ -22,6 +22,7 @@
 
 #include "db_internal.h"
 #include "dev_common.cuh"
+#include "xsum.cuh"
 #include "tail.cuh"
 
 namespace db {
@@ -159,6 +160,16 @@ __global__ void __launch_bounds__(PREP_THREADS) k_prep(Geom g, Inputs in, Accum 
     const ulonglong2 ident = make_ulonglong2(~0ull, ~0ull);
     for (int64_t i = t0; i < (int64_t)(nb * acc.nmm); i += stride) ((ulonglong2 *)acc.mm)[i] = ident;
     if (t0 < 2 * g.ndim) acc.bounds[t0] = ~0ull;
+    if (acc.xs) {  // exact sums: clear the digits the slot's previous execute touched (the
+                   // range itself is reset by a stream-ordered memset after this kernel)
+        for (int s = 0; s < acc.nsum; ++s) {
+            const int klo = acc.xrange[2 * s], khi = -acc.xrange[2 * s + 1];
+            if (klo == XR_EMPTY || klo > khi) continue;
+            long long *d = acc.xs + ((uint64_t)s * XD + klo) * nb;
+            const int64_t m = (int64_t)(khi - klo + 1) * (int64_t)nb;
+            for (int64_t i = t0; i < m; i += stride) d[i] = 0ll;
+        }
+    }
 }
 
 __global__ void __launch_bounds__(PREP_THREADS) k_window(Geom g, Inputs in, Accum acc, int wcap) {

@@ -216,6 +216,8 @@ int bin_multi_init(const bin_multi_op_t *ops, int32_t nops, int32_t ncols, const
             const std::string msg = bin_last_error();
             return set_error(rc, "instance %d: %s", k, msg.c_str());
         }
+        if (ops[k].spec.sum_mode == BIN_SUM_EXACT)
+            return set_error(BIN_ENOTSUP, "instance %d: BIN_SUM_EXACT is not fused (use bin_init)", k);
         if (ops[k].spec.deterministic)
             return set_error(BIN_ENOTSUP, "instance %d: deterministic mode is not fused (use bin_init)", k);
         int ns = 0, nm = 0;

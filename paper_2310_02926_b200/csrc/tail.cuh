@@ -8,16 +8,40 @@
 
 #include "db_internal.h"
 #include "dev_common.cuh"
+#include "xsum.cuh"
 
 namespace db {
 
 // ---------------------------------------------------------------- finalize [a7]
+// BIN_SUM_EXACT: a bin's sum is its digit row rounded once (xsum.cuh), written
+// into the sum output, then divided for the average.
+__device__ __forceinline__ double exact_sum_of(const Accum &acc, int s, uint64_t b, unsigned long long cnt) {
+    if (!cnt) return 0.0;
+    const int klo = __ldcg(acc.xrange + 2 * s), nkhi = __ldcg(acc.xrange + 2 * s + 1);
+    if (klo == XR_EMPTY) return 0.0;
+    return xsum_round(acc.xs, acc.nbins, s, b, klo, -nkhi);
+}
+
 __device__ __forceinline__ void finalize_body(const Geom &g, const Accum &acc, Meta *meta, int variant) {
     DGeom G = load_geom(g, acc.bounds);
     const uint64_t nb = acc.nbins;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (G.ok && acc.nsum <= 1 && acc.nmm <= 1) {
+    if (G.ok && acc.xs) {
+        for (int64_t b = t0; b < (int64_t)nb; b += stride) {
+            const unsigned long long cnt = __ldcg(acc.count + b);
+            for (int s = 0; s < acc.nsum; ++s) {
+                const double sm = exact_sum_of(acc, s, (uint64_t)b, cnt);
+                acc.sum[(uint64_t)s * nb + b] = sm;
+                acc.oavg[(uint64_t)s * nb + b] = cnt ? __ddiv_rn(sm, (double)cnt) : __longlong_as_double(0x7ff8000000000000ll);
+            }
+            for (int s = 0; s < acc.nmm; ++s) {
+                const ulonglong2 m = __ldcg((const ulonglong2 *)acc.mm + (uint64_t)s * nb + b);
+                acc.omin[(uint64_t)s * nb + b] = cnt ? dec_total(m.x) : __longlong_as_double(0x7ff0000000000000ll);
+                acc.omax[(uint64_t)s * nb + b] = cnt ? dec_total(~m.y) : __longlong_as_double((long long)0xfff0000000000000ull);
+            }
+        }
+    } else if (G.ok && acc.nsum <= 1 && acc.nmm <= 1) {
         // common case: issue the bin's loads together (one latency, not three)
         for (int64_t b = t0; b < (int64_t)nb; b += stride) {
             const unsigned long long cnt = __ldcg(acc.count + b);

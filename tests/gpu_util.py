@@ -19,7 +19,8 @@ def bits(x):
 
 
 def run_gpu(db, axes, attrs, res, lo=None, hi=None, ops=ALL_OPS, bounds_auto=False, deterministic=False,
-            placement=None, offset=0, host_inputs=False, device=0, return_handle=False, route="auto"):
+            placement=None, offset=0, host_inputs=False, device=0, return_handle=False, route="auto",
+            exact=False):
     import torch
     dev = torch.device(f"cuda:{device}")
     cols = list(axes) + list(attrs)
@@ -38,7 +39,7 @@ def run_gpu(db, axes, attrs, res, lo=None, hi=None, ops=ALL_OPS, bounds_auto=Fal
         handles.append(db.wrap_tensor(t))
     torch.cuda.synchronize(dev)
     spec = db.make_spec(res, lo, hi, nattr=len(attrs), ops=ops, bounds_auto=bounds_auto,
-                        deterministic=deterministic, route=route)
+                        deterministic=deterministic, route=route, exact=exact)
     pl = placement if placement is not None else db.make_placement(device_id=device)
     h = db.bin_init(spec, pl)
     db.bin_profile_enable(h, True)
