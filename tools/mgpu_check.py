@@ -56,11 +56,12 @@ def main():
         torch.cuda.synchronize(dev)
         hs = [db.wrap_tensor(t) for t in cols]
         D = len(w.axes)
-        for det, route in ((False, "auto"), (False, "window"), (False, "partition"), (True, "auto")):
+        for det, route, exact in ((False, "auto", False), (False, "window", False), (False, "partition", False),
+                                  (True, "auto", False), (False, "auto", True), (False, "partition", True)):
             obj = [db.bin_nccl_unique_id() if rank == 0 else None]
             dist.broadcast_object_list(obj, src=0)
             spec = db.make_spec(res, None if auto else w.lo, None if auto else w.hi, nattr=len(w.attrs),
-                                ops=w.ops, bounds_auto=auto, deterministic=det, route=route)
+                                ops=w.ops, bounds_auto=auto, deterministic=det, route=route, exact=exact)
             h = db.bin_init(spec, db.make_placement(), rank=rank, nranks=world, nccl_id=obj[0])
             db.bin_profile_enable(h, True)
             t = db.bin_execute(h, hs[:D], hs[D:])
@@ -72,16 +73,22 @@ def main():
                 axes = [synth.fill_host(w.dist, w.central, w.seed, synth.COLUMNS[c], 0, n) for c in w.axes]
                 attrs = [synth.fill_host(w.dist, w.central, w.seed, synth.COLUMNS[c], 0, n) for c in w.attrs]
                 ref = oracle.databin(axes, attrs, res, None if auto else w.lo, None if auto else w.hi,
-                                     bounds_auto=auto, P=world if det else 1)
+                                     bounds_auto=auto, P=world if det else 1, exact=exact)
                 status = "ok"
                 try:
                     compare(out, ref, w.ops, exact=det)
+                    if exact:  # exact sums: bit-identical to the once-rounded exact sum for any rank count
+                        for a in range(len(w.attrs)):
+                            assert np.array_equal(out["sum"][a].view(np.uint64), ref["sum_exact"][a].view(np.uint64))
+                            occ = ref["count"] > 0
+                            assert np.array_equal(out["avg"][a][occ].view(np.uint64),
+                                                  ref["avg_exact"][a][occ].view(np.uint64))
                     if auto:
                         assert np.array_equal(out["lo"], ref["lo"]) and np.array_equal(out["hi"], ref["hi"])
                 except AssertionError as e:  # noqa: PERF203
                     status = "FAIL: " + str(e)[:300]
                     ok = False
-                print(json.dumps({"case": name, "deterministic": det, "route": route, "variant": variant,
+                print(json.dumps({"case": name, "deterministic": det, "exact": exact, "route": route, "variant": variant,
                                   "world": world, "rows": n,
                                   "res": list(res), "status": status, "n_in": out["n_in"],
                                   "n_out": out["n_out"]}), flush=True)
