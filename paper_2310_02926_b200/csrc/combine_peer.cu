@@ -32,10 +32,11 @@ namespace db {
 
 constexpr int COMB_THREADS = 256;
 
+template <bool EXACT>
 __global__ void __launch_bounds__(COMB_THREADS) k_combine_peer(Geom g, PeerSet ps, int rank, int nranks,
                                                                unsigned long long epoch, Meta *meta, int variant,
                                                                int bulk) {
-    combine_peer_body(g, ps, rank, nranks, epoch, meta, variant, bulk != 0);
+    combine_peer_body<EXACT>(g, ps, rank, nranks, epoch, meta, variant, bulk != 0);
 }
 
 // dynamic shared memory of the bulk slice: NR ranks x 4 words + 5 output words per bin
@@ -47,12 +48,13 @@ cudaError_t launch_combine_peer(const Geom &g, const PeerSet &ps, int rank, int 
     const uint64_t slice = (B + nranks - 1) / nranks;
     (void)deterministic;
     static const bool no_bulk = getenv("DATABIN_COMBINE_BULK") && getenv("DATABIN_COMBINE_BULK")[0] == '0';
-    const bool bulk = !no_bulk && ps.me.nsum <= 1 && ps.me.nmm <= 1 && (nranks == 2 || nranks == 4 || nranks == 8);
+    const bool bulk = !no_bulk && !ps.me.xs && ps.me.nsum <= 1 && ps.me.nmm <= 1 &&
+                      (nranks == 2 || nranks == 4 || nranks == 8);
     uint64_t blocks;
     size_t smem = 0;
     if (bulk) {
         smem = combine_bulk_smem(nranks);
-        cudaError_t e = cudaFuncSetAttribute(k_combine_peer, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaError_t e = cudaFuncSetAttribute(k_combine_peer<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         blocks = (slice + COMB_CB - 1) / COMB_CB;  // one chunk of COMB_CB bins per CTA and step
         if (blocks > (uint64_t)sms * 4) blocks = (uint64_t)sms * 4;
@@ -61,7 +63,11 @@ cudaError_t launch_combine_peer(const Geom &g, const PeerSet &ps, int rank, int 
         if (blocks > (uint64_t)sms * 8) blocks = (uint64_t)sms * 8;
     }
     if (blocks < 1) blocks = 1;
-    k_combine_peer<<<(unsigned)blocks, COMB_THREADS, smem, s>>>(g, ps, rank, nranks, epoch, meta, variant, bulk ? 1 : 0);
+    if (ps.me.xs)
+        k_combine_peer<true><<<(unsigned)blocks, COMB_THREADS, smem, s>>>(g, ps, rank, nranks, epoch, meta, variant, 0);
+    else
+        k_combine_peer<false><<<(unsigned)blocks, COMB_THREADS, smem, s>>>(g, ps, rank, nranks, epoch, meta, variant,
+                                                                           bulk ? 1 : 0);
     return cudaGetLastError();
 }
 

@@ -179,6 +179,8 @@ struct PeerSet {
     double *sum[PEER_MAX];
     unsigned long long *mm[PEER_MAX];
     double *omin[PEER_MAX], *omax[PEER_MAX], *oavg[PEER_MAX];
+    long long *xs[PEER_MAX];              // BIN_SUM_EXACT: every rank's digit rows and ranges
+    int32_t *xrange[PEER_MAX];
     unsigned long long *flags[PEER_MAX];  // every rank's barrier words [A: 0..63][B: 64..127]
     unsigned *ctas_done;                  // this rank's last-CTA counter
 };

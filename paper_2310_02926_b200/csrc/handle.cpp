@@ -398,6 +398,8 @@ static bool setup_peer(bin_handle *h) {
             ps.omin[p] = (double *)rel(S.acc.omin, p);
             ps.omax[p] = (double *)rel(S.acc.omax, p);
             ps.oavg[p] = (double *)rel(S.acc.oavg, p);
+            ps.xs[p] = S.acc.xs ? (long long *)rel(S.acc.xs, p) : nullptr;
+            ps.xrange[p] = S.acc.xrange ? (int32_t *)rel(S.acc.xrange, p) : nullptr;
             ps.flags[p] = flags[p];
         }
     }
@@ -511,7 +513,7 @@ int bin_init(const bin_spec_t *spec, const bin_placement_t *place, const bin_com
             h->comm = nullptr;
             return fail(nccl_error(r, "ncclCommInitRank"));
         }
-        h->peer = h->spec.sum_mode != BIN_SUM_EXACT && setup_peer(h);  // exact: digits go through NCCL
+        h->peer = setup_peer(h);
     }
     *out = h;
     return BIN_OK;

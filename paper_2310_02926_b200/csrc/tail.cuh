@@ -276,6 +276,7 @@ __device__ void combine_slice_bulk(const PeerSet &ps, uint64_t e0, uint64_t e1, 
 
 // bulk: the slice uses TMA bulk copies (the kernel was launched with
 // combine_bulk_smem(nranks) bytes of dynamic shared memory)
+template <bool EXACT>
 __device__ __forceinline__ void combine_peer_body(const Geom &g, const PeerSet &ps, int rank, int nranks,
                                                   unsigned long long epoch, Meta *meta, int variant, bool bulk) {
     __shared__ bool ok_s, last_s;
@@ -299,12 +300,35 @@ __device__ __forceinline__ void combine_peer_body(const Geom &g, const PeerSet &
     const double qnan = __longlong_as_double(0x7ff8000000000000ll);
     const double pinf = __longlong_as_double(0x7ff0000000000000ll);
     const double ninf = __longlong_as_double((long long)0xfff0000000000000ull);
+    // exact sums: the union of the ranks' touched digit ranges, per summed attribute
+    __shared__ int s_klo[BIN_MAX_ATTR], s_khi[BIN_MAX_ATTR];
+    constexpr bool exact = EXACT;  // (a separate instance: the fast combine carries no digit code)
+    if (exact && threadIdx.x < nsum) {
+        int lo = XR_EMPTY, nhi = XR_EMPTY;
+        for (int p = 0; p < nranks; ++p) {
+            lo = min(lo, __ldcg(ps.xrange[p] + 2 * threadIdx.x));
+            nhi = min(nhi, __ldcg(ps.xrange[p] + 2 * threadIdx.x + 1));
+        }
+        s_klo[threadIdx.x] = lo == XR_EMPTY ? 1 : lo;
+        s_khi[threadIdx.x] = lo == XR_EMPTY ? 0 : -nhi;
+    }
+    if (exact) __syncthreads();
     auto generic = [&](uint64_t b) {
         unsigned long long cnt = 0;
         for (int p = 0; p < nranks; ++p) cnt += __ldcg(ps.count[p] + b);
         for (int q = 0; q < nranks; ++q) ps.count[q][b] = cnt;
         for (int s = 0; s < nsum; ++s) {
             double sm = 0.0;  // rank-order fold from +0.0 (oracle partition mode)
+            if constexpr (EXACT) {  // digits add as integers over the ranks, then one rounding
+                long long d[XD];
+                const int klo = s_klo[s], khi = s_khi[s];
+                for (int k = klo; k <= khi; ++k) {
+                    long long a = 0;
+                    for (int p = 0; p < nranks; ++p) a += __ldcg(ps.xs[p] + ((uint64_t)s * XD + k) * B + b);
+                    d[k - klo] = a;
+                }
+                sm = cnt ? xsum_round_digits(d, klo, khi) : 0.0;
+            } else
             for (int p = 0; p < nranks; ++p) sm = __dadd_rn(sm, __ldcg(ps.sum[p] + (uint64_t)s * B + b));
             const double avg = cnt ? __ddiv_rn(sm, (double)cnt) : qnan;
             for (int q = 0; q < nranks; ++q) {
@@ -327,7 +351,7 @@ __device__ __forceinline__ void combine_peer_body(const Geom &g, const PeerSet &
         }
     };
     // fast path (common case): NR lanes per bin; else the generic per-bin loop
-    const bool fastp = ok && nsum <= 1 && nmm <= 1 && (nranks == 2 || nranks == 4 || nranks == 8);
+    const bool fastp = ok && !exact && nsum <= 1 && nmm <= 1 && (nranks == 2 || nranks == 4 || nranks == 8);
     if (bulk && fastp) {  // TMA bulk copies for the even-aligned body; the <= 2 edge bins below
         const uint64_t e0 = (s0 + 1) & ~1ull, e1 = s1 & ~1ull;
         if (e0 < e1) {

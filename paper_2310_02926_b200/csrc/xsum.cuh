@@ -118,15 +118,16 @@ __device__ __forceinline__ bool x_sticky(const unsigned *u, int L, int base, int
     return false;
 }
 
-// The exact value of digit row (slot, b) over digits [klo, khi], rounded once
-// to the nearest double (ties to even); +-inf beyond DBL_MAX; zero -> +0.0.
-__device__ __noinline__ static double xsum_round(const long long *xs, uint64_t B, int slot, uint64_t b, int klo, int khi) {
+// The exact value sum_k d[k - klo] * 2^(32k) (units 2^-1074) of the digits
+// [klo, khi], rounded once to the nearest double (ties to even); +-inf beyond
+// DBL_MAX; zero -> +0.0.
+__device__ __noinline__ static double xsum_round_digits(const long long *d, int klo, int khi) {
     if (klo > khi) return 0.0;
     unsigned u[XD + 4];
     long long carry = 0;
     int L = 0;
     for (int k = klo; k <= khi; ++k) {
-        const long long t = __ldcg(xs + ((uint64_t)slot * XD + k) * B + b) + carry;
+        const long long t = d[k - klo] + carry;
         u[L++] = (unsigned)t;
         carry = t >> 32;  // arithmetic: the signed carry into the next digit
     }
@@ -166,6 +167,13 @@ __device__ __noinline__ static double xsum_round(const long long *xs, uint64_t B
     }
     if (neg) out |= 1ull << 63;
     return __longlong_as_double((long long)out);
+}
+
+// Digit row (slot, b) of one rank's accumulator, rounded once.
+__device__ __forceinline__ double xsum_round(const long long *xs, uint64_t B, int slot, uint64_t b, int klo, int khi) {
+    long long d[XD];
+    for (int k = klo; k <= khi; ++k) d[k - klo] = __ldcg(xs + ((uint64_t)slot * XD + k) * B + b);
+    return xsum_round_digits(d, klo, khi);
 }
 
 }  // namespace db
