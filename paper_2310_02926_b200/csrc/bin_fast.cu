@@ -34,6 +34,24 @@ enum : uint32_t { QK_GLOBAL = 1u, QK_MIN = 2u, QK_MAX = 4u };
 
 int fast_queue_bytes() { return (FAST_THREADS / 32) * QWORDS * 4 + 16; }
 
+// Shared-memory window accesses through 32-bit shared-window addresses from one
+// base register (BIN_SADDR=1): generic atomics on the extern array made the
+// compiler re-derive the window base (S2R SR_CgaCtaId + LEA) for every row.
+#ifndef BIN_SADDR
+#define BIN_SADDR 1
+#endif
+__device__ __forceinline__ void s_red_add(uint32_t a, uint32_t v) {
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a), "r"(v));
+}
+__device__ __forceinline__ uint32_t s_atom_add(uint32_t a, uint32_t v) {
+    uint32_t r;
+    asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(r) : "r"(a), "r"(v));
+    return r;
+}
+__device__ __forceinline__ void s_red_min(uint32_t a, uint32_t v) {
+    asm volatile("red.shared.min.u32 [%0], %1;" ::"r"(a), "r"(v));
+}
+
 // Hot-loop context: only the D used dimensions (so it stays in registers).
 template <int D>
 struct FastCtx {
@@ -44,6 +62,7 @@ struct FastCtx {
     uint32_t W;
     FxParam fx;
     uint32_t o_fx, o_cnt;  // word offsets (filters at 0)
+    uint32_t sb;           // shared-window address of f_dsm[0]
 };
 
 template <int D, int A, int SM, int MM>
@@ -71,7 +90,8 @@ __device__ __forceinline__ uint32_t fast_row(const FastCtx<D> &c, const double (
     if (D >= 2) b += (uint32_t)(c.resm1[0] + 1) * (uint32_t)k[1];
     if (D >= 3) b += (uint32_t)(c.resm1[0] + 1) * (uint32_t)(c.resm1[D > 2 ? 1 : 0] + 1) * (uint32_t)k[D > 2 ? 2 : 0];
     if (!inw) return (QK_GLOBAL << 29) | b;
-    atomicAdd(&f_dsm[c.o_cnt + l], 1u);
+    if (BIN_SADDR) s_red_add(c.sb + 4u * (c.o_cnt + l), 1u);
+    else atomicAdd(&f_dsm[c.o_cnt + l], 1u);
     const uint32_t W = c.W;
     uint32_t tag = 0;
     if (HS) {
@@ -81,28 +101,38 @@ __device__ __forceinline__ uint32_t fast_row(const FastCtx<D> &c, const double (
             const unsigned long long q = fx_quant(c.fx, v);
             const unsigned qlo = (unsigned)q;
             qmid = (unsigned)(q >> 32);
-            const unsigned old = atomicAdd(&f_dsm[w0], qlo);
+            const unsigned old = BIN_SADDR ? s_atom_add(c.sb + 4u * w0, qlo) : atomicAdd(&f_dsm[w0], qlo);
             qmid += (old + qlo < old) ? 1u : 0u;
         } else {  // rare: outside the fixed range -> sum (and min/max) go global; count stays here
             tag = ((QK_GLOBAL | QK_MIN) << 29) | b;
             qmid = FX_OFFSET_MID;
         }
-        const unsigned old2 = atomicAdd(&f_dsm[w0 + W], qmid);
-        if (old2 + qmid < old2) atomicAdd(&f_dsm[w0 + 2 * W], 1u);
+        const unsigned old2 = BIN_SADDR ? s_atom_add(c.sb + 4u * (w0 + W), qmid) : atomicAdd(&f_dsm[w0 + W], qmid);
+        if (old2 + qmid < old2) {
+            if (BIN_SADDR) s_red_add(c.sb + 4u * (w0 + 2 * W), 1u);
+            else atomicAdd(&f_dsm[w0 + 2 * W], 1u);
+        }
     }
     if (HM && tag == 0) {
         const unsigned long long e = enc_total(v);
         const unsigned eh = (unsigned)(e >> 32), neh = ~eh;
         uint2 f;  // one LDS.64; stale values are safe (the words only decrease)
-        asm volatile("ld.volatile.shared.v2.u32 {%0, %1}, [%2];" : "=r"(f.x), "=r"(f.y) : "r"((unsigned)__cvta_generic_to_shared(&f_dsm[2 * l])));
+        const uint32_t fa = BIN_SADDR ? c.sb + 8u * l : (unsigned)__cvta_generic_to_shared(&f_dsm[2 * l]);
+        asm volatile("ld.volatile.shared.v2.u32 {%0, %1}, [%2];" : "=r"(f.x), "=r"(f.y) : "r"(fa));
         uint32_t kind = 0;
         if (eh <= f.x) {
             kind |= QK_MIN;
-            if (eh < f.x) atomicMin(&f_dsm[2 * l], eh);
+            if (eh < f.x) {
+                if (BIN_SADDR) s_red_min(fa, eh);
+                else atomicMin(&f_dsm[2 * l], eh);
+            }
         }
         if (neh <= f.y) {
             kind |= QK_MAX;
-            if (neh < f.y) atomicMin(&f_dsm[2 * l + 1], neh);
+            if (neh < f.y) {
+                if (BIN_SADDR) s_red_min(fa + 4u, neh);
+                else atomicMin(&f_dsm[2 * l + 1], neh);
+            }
         }
         if (kind) tag = (kind << 29) | b;
     }
@@ -333,6 +363,10 @@ __global__ void __launch_bounds__(FAST_THREADS, 1)
     const uint32_t W = c.W;
     c.o_fx = HM ? 2u * W : 0u;
     c.o_cnt = c.o_fx + (HS ? 3u * W : 0u);
+    {  // opaque copy: keeps the base in a register instead of re-deriving it per row
+        const uint32_t sb0 = (uint32_t)__cvta_generic_to_shared(f_dsm);
+        asm volatile("mov.b32 %0, %1;" : "=r"(c.sb) : "r"(sb0));
+    }
 
     for (uint32_t i = threadIdx.x; i < c.o_fx; i += FAST_THREADS) f_dsm[i] = ~0u;  // min/max filters
     const uint32_t o_end = c.o_cnt + W;
