@@ -259,6 +259,23 @@ int bin_init(const bin_spec_t *spec, const bin_placement_t *place,
 int bin_execute(bin_handle_t *h, bin_array_t *const *axes, int32_t naxes,
                 bin_array_t *const *attrs, int32_t nattr, uint64_t *ticket);
 
+/* Fan-in execute (the paper's "dedicated device" placement, PAPER.md:496-497:
+ * "Data is moved from the three simulation GPUs ... to the one in situ GPU"):
+ * bins nshards row blocks -- e.g. the arrays of several producer GPUs -- as ONE
+ * batch into one result.  Shard s's columns are axes[s*naxes + d] and
+ * attrs[s*nattr + a]; columns agree in length within a shard, shards may
+ * differ in length and live anywhere (host, this GPU, other GPUs).  Every
+ * column is staged on the handle's copy stream into one buffer, shard after
+ * shard (NVLink peer copies from other GPUs run concurrently with the
+ * previous execute), each copy ordered after its producer stream's pending
+ * work; then the execute proceeds as bin_execute over the concatenated rows
+ * (deterministic mode folds them in shard order).  nshards == 1 is
+ * bin_execute.  Errors: as bin_execute; BIN_EINVAL for nshards outside
+ * 1..BIN_MAX_SHARDS. */
+#define BIN_MAX_SHARDS 64
+int bin_execute_shards(bin_handle_t *h, bin_array_t *const *axes, int32_t naxes,
+                       bin_array_t *const *attrs, int32_t nattr, int32_t nshards, uint64_t *ticket);
+
 /* Event after which the producer may overwrite the inputs of `ticket`
  * (snapshot copy done, or binning done when reading in place). */
 int bin_inputs_released(bin_handle_t *h, uint64_t ticket, bin_event_t *ev);

@@ -153,6 +153,19 @@ def bin_execute(h, axes, attrs):
     return t.value
 
 
+def bin_execute_shards(h, shards):
+    """shards: list of (axes, attrs) handle lists, one per row block (fan-in)."""
+    ax = [a for axes, _ in shards for a in axes]
+    at = [a for _, attrs in shards for a in attrs]
+    naxes, nattr = len(shards[0][0]), len(shards[0][1])
+    axa = (ctypes.c_void_p * max(1, len(ax)))(*ax)
+    ata = (ctypes.c_void_p * max(1, len(at)))(*at)
+    t = ctypes.c_uint64()
+    check(_lib.bin_execute_shards(ctypes.c_void_p(h), axa, naxes, ata, nattr, len(shards), ctypes.byref(t)),
+          "bin_execute_shards")
+    return t.value
+
+
 def bin_inputs_released(h, ticket):
     ev = ctypes.c_void_p()
     check(_lib.bin_inputs_released(ctypes.c_void_p(h), ticket, ctypes.byref(ev)), "bin_inputs_released")

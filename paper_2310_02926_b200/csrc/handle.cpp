@@ -557,22 +557,36 @@ static int run_probe(bin_handle *h, const Geom &geom, const Inputs &in, Slot &S,
     return BIN_OK;
 }
 
-int bin_execute(bin_handle_t *h, bin_array_t *const *axes, int32_t naxes, bin_array_t *const *attrs,
-                int32_t nattr, uint64_t *ticket) {
+// One execute over nshards row blocks (nshards == 1: bin_execute).  Shard s's
+// columns are axes[s * ndim + d] and attrs[s * nattr + a].  With several shards
+// every column is staged into one buffer, shard after shard (host: H2D; other
+// GPU: NVLink peer copy; this GPU: D2D), and binned as one batch.
+static int execute_impl(bin_handle *h, bin_array_t *const *axes, int32_t naxes, bin_array_t *const *attrs,
+                        int32_t nattr, int32_t nshards, uint64_t *ticket) {
     if (!h || h->finalized) return set_error(BIN_ESTATE, "bin_execute: handle is NULL or finalized");
     if (naxes != h->spec.ndim) return set_error(BIN_ESHAPE, "%d axis columns for a %dD mesh", naxes, h->spec.ndim);
     if (nattr != h->spec.nattr) return set_error(BIN_ESHAPE, "%d attribute columns, spec has %d", nattr, h->spec.nattr);
+    if (nshards < 1 || nshards > BIN_MAX_SHARDS)
+        return set_error(BIN_EINVAL, "%d shards (1..%d)", nshards, BIN_MAX_SHARDS);
     bin_array *cols[BIN_MAX_DIM + BIN_MAX_ATTR];
-    int ncols = naxes + nattr;
-    for (int i = 0; i < ncols; ++i) {
-        cols[i] = i < naxes ? axes[i] : attrs[i - naxes];
-        if (!cols[i]) return set_error(BIN_EINVAL, "column %d is NULL", i);
-        if (cols[i]->dtype != BIN_F64) return set_error(BIN_EDTYPE, "column %d is not BIN_F64", i);
-        if (cols[i]->n != cols[0]->n)
-            return set_error(BIN_ESHAPE, "column %d has %lld rows, column 0 has %lld", i, (long long)cols[i]->n,
-                             (long long)cols[0]->n);
+    const int ncols = naxes + nattr;
+    int64_t shard_n[BIN_MAX_SHARDS];
+    int64_t n = 0;
+    for (int sh = 0; sh < nshards; ++sh) {
+        bin_array *c0 = nullptr;
+        for (int i = 0; i < ncols; ++i) {
+            bin_array *c = i < naxes ? axes[sh * naxes + i] : attrs[sh * nattr + i - naxes];
+            if (!c) return set_error(BIN_EINVAL, "shard %d column %d is NULL", sh, i);
+            if (c->dtype != BIN_F64) return set_error(BIN_EDTYPE, "shard %d column %d is not BIN_F64", sh, i);
+            if (!c0) c0 = c;
+            if (c->n != c0->n)
+                return set_error(BIN_ESHAPE, "shard %d: column %d has %lld rows, column 0 has %lld", sh, i,
+                                 (long long)c->n, (long long)c0->n);
+        }
+        shard_n[sh] = c0->n;
+        n += c0->n;
     }
-    const int64_t n = cols[0]->n;
+    for (int i = 0; i < ncols; ++i) cols[i] = i < naxes ? axes[i] : attrs[i - naxes];  // shard 0 (ordering, mode)
     DeviceGuard g(h->device);
     const uint64_t t = h->next_ticket++;
     const int sl = (int)(t & 1);
@@ -619,11 +633,45 @@ int bin_execute(bin_handle_t *h, bin_array_t *const *axes, int32_t naxes, bin_ar
     for (int i = 0; i < ncols; ++i) {
         bin_array *a = cols[i];
         const bool local = a->alloc == BIN_ALLOC_CUDA_UVA || (is_device_memory(a) && a->device == h->device);
-        stage[i] = n > 0 && (!local || snapshot);
+        stage[i] = n > 0 && (!local || snapshot || nshards > 1);
         staged_any = staged_any || stage[i];
     }
     if (staged_any && S.used) DB_CUDA(cudaStreamWaitEvent(h->copy, S.done, 0));  // staging buffers free again
-    for (int i = 0; i < ncols; ++i) {
+    if (nshards > 1) {  // fan-in: every column concatenated shard after shard into one staging buffer
+        for (int i = 0; i < ncols && n > 0; ++i) {
+            void *dst = nullptr;
+            int rc0 = stage_buffer(h, sl, i, (size_t)n * 8, &dst);
+            if (rc0) return rc0;
+            int64_t off = 0;
+            for (int sh = 0; sh < nshards; ++sh) {
+                bin_array *a = i < naxes ? axes[sh * naxes + i] : attrs[sh * nattr + i - naxes];
+                const size_t bytes = (size_t)shard_n[sh] * 8;
+                if (a->device >= 0 || a->alloc == BIN_ALLOC_HOST_PINNED) {  // after the producer's pending work
+                    const int pd = a->device >= 0 ? a->device : h->device;
+                    DeviceGuard g2(pd);
+                    cudaEvent_t tmp;
+                    DB_CUDA(cudaEventCreateWithFlags(&tmp, cudaEventDisableTiming));
+                    DB_CUDA(cudaEventRecord(tmp, a->stream));
+                    DeviceGuard g3(h->device);
+                    DB_CUDA(cudaStreamWaitEvent(h->copy, tmp, 0));
+                    cudaEventDestroy(tmp);
+                }
+                unsigned char *d = (unsigned char *)dst + (size_t)off * 8;
+                if (bytes) {
+                    if (a->device == -1 || a->alloc == BIN_ALLOC_HOST || a->alloc == BIN_ALLOC_HOST_PINNED)
+                        DB_CUDA(cudaMemcpyAsync(d, a->ptr, bytes, cudaMemcpyHostToDevice, h->copy));
+                    else if (a->device != h->device && a->alloc != BIN_ALLOC_CUDA_UVA)
+                        DB_CUDA(cudaMemcpyPeerAsync(d, h->device, a->ptr, a->device, bytes, h->copy));
+                    else
+                        DB_CUDA(cudaMemcpyAsync(d, a->ptr, bytes, cudaMemcpyDeviceToDevice, h->copy));
+                }
+                off += shard_n[sh];
+            }
+            if (i < naxes) in.ax[i] = (const double *)dst;
+            else in.at[i - naxes] = (const double *)dst;
+        }
+    }
+    for (int i = 0; i < ncols && nshards == 1; ++i) {
         bin_array *a = cols[i];
         const double *p = (const double *)a->ptr;
         cudaStream_t consumer = stage[i] ? h->copy : s;
@@ -837,14 +885,27 @@ int bin_execute(bin_handle_t *h, bin_array_t *const *axes, int32_t naxes, bin_ar
     DB_CUDA(cudaEventRecord(S.done, s));
     if (!staged_any) DB_CUDA(cudaEventRecord(S.released, s));
     S.prof_pending = h->prof;
-    for (int i = 0; i < ncols; ++i)
-        if ((rc = array_mark_use(cols[i], s, h->device))) return rc;
+    for (int sh = 0; sh < nshards; ++sh)
+        for (int i = 0; i < ncols; ++i) {
+            bin_array *a = i < naxes ? axes[sh * naxes + i] : attrs[sh * nattr + i - naxes];
+            if ((rc = array_mark_use(a, s, h->device))) return rc;
+        }
     if (ticket) *ticket = t;
     if (h->place.exec == BIN_EXEC_SYNC && cols[0]->mode == BIN_SYNC) {
         e = cudaEventSynchronize(S.done);
         if (e != cudaSuccess) return cuda_error(e, "bin_execute (lockstep) synchronize");
     }
     return BIN_OK;
+}
+
+int bin_execute(bin_handle_t *h, bin_array_t *const *axes, int32_t naxes, bin_array_t *const *attrs,
+                int32_t nattr, uint64_t *ticket) {
+    return execute_impl(h, axes, naxes, attrs, nattr, 1, ticket);
+}
+
+int bin_execute_shards(bin_handle_t *h, bin_array_t *const *axes, int32_t naxes, bin_array_t *const *attrs,
+                       int32_t nattr, int32_t nshards, uint64_t *ticket) {
+    return execute_impl(h, axes, naxes, attrs, nattr, nshards, ticket);
 }
 
 static Slot *find_slot(bin_handle *h, uint64_t t) {

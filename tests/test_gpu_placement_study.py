@@ -14,8 +14,8 @@ def test_placement_modes_agree_and_do_not_interfere(cuda_available):
     import torch
 
     from tools import placement_study as ps
-    modes = [m for m in ps.MODES if m != "peer" or torch.cuda.device_count() > 1]
-    results = [ps.run_mode(m, 1_000_003, 6) for m in modes]
+    modes = [m for m in ps.MODES if m not in ("peer", "fanin") or torch.cuda.device_count() > 1]
+    results = [ps.run_fanin(1_000_003, 6) if m == "fanin" else ps.run_mode(m, 1_000_003, 6) for m in modes]
     assert ps.check(results)
     for m, _, _ in results:
         assert m["solver_ms_per_step"] > 0 and m["actual_insitu_ms_per_step"] > 0
