@@ -52,8 +52,8 @@ def _load():
                                             ctypes.c_uint64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int]
             lib.synth_fill_device.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.c_int,
                                               ctypes.c_uint64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]
-            lib.synth_kdk_step.argtypes = [ctypes.c_void_p] * 6 + [ctypes.c_int64, ctypes.c_double, ctypes.c_double,
-                                                                   ctypes.c_double, ctypes.c_void_p]
+            lib.synth_kdk_step.argtypes = [ctypes.c_void_p] * 6 + [ctypes.c_int64, ctypes.c_int64, ctypes.c_double,
+                                                                   ctypes.c_double, ctypes.c_double, ctypes.c_void_p]
             _lib = lib
     return _lib
 
@@ -71,10 +71,11 @@ def fill_device(dist, central, seed, column, start, n, dptr, stream=0) -> None:
         raise RuntimeError(f"synth_fill_device: cudaError {rc}")
 
 
-def kdk_step(cols, n, stream=0, central_mass=1000.0, eps2=1e-4, dt=1e-5):
+def kdk_step(cols, n, stream=0, central_mass=1000.0, eps2=1e-4, dt=1e-5, start=0):
     """One leapfrog step of the placement-study producer on device columns
-    (x, y, z, vx, vy, vz as device pointers); see synth.cu syn_kdk_kernel."""
-    rc = _load().synth_kdk_step(*[ctypes.c_void_p(c) for c in cols], int(n), central_mass, eps2, dt,
+    (x, y, z, vx, vy, vz as device pointers) holding global rows start..start+n-1;
+    see synth.cu syn_kdk_kernel."""
+    rc = _load().synth_kdk_step(*[ctypes.c_void_p(c) for c in cols], int(n), int(start), central_mass, eps2, dt,
                                 ctypes.c_void_p(stream))
     if rc != 0:
         raise RuntimeError(f"synth_kdk_step: cudaError {rc}")

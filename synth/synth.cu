@@ -21,11 +21,11 @@ __global__ void syn_fill_kernel(int dist, int central, uint64_t seed, int column
 // scope); it reads 7 and writes 6 columns per body (104 B), like a solver
 // step's streaming cost.  Not part of the binning method.
 __global__ void syn_kdk_kernel(double *x, double *y, double *z, double *vx, double *vy, double *vz, int64_t n,
-                               double central_mass, double eps2, double dt) {
+                               int64_t start, double central_mass, double eps2, double dt) {
     const double hdt = 0.5 * dt;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-        if (i == 0) continue;  // the massive body stays at the origin
+        if (start + i == 0) continue;  // the massive body (global row 0) stays at the origin
         double px = x[i], py = y[i], pz = z[i], ux = vx[i], uy = vy[i], uz = vz[i];
         double r2 = SYN_ADD(SYN_ADD(SYN_ADD(SYN_MUL(px, px), SYN_MUL(py, py)), SYN_MUL(pz, pz)), eps2);
         double inv = SYN_DIV(central_mass, SYN_MUL(r2, SYN_SQRT(r2)));
@@ -48,8 +48,8 @@ __global__ void syn_kdk_kernel(double *x, double *y, double *z, double *vx, doub
 
 extern "C" {
 
-// One KDK step of n bodies (device columns), enqueued on `stream`.
-int synth_kdk_step(double *x, double *y, double *z, double *vx, double *vy, double *vz, int64_t n,
+// One KDK step of n bodies (device columns; row 0 is global row `start`), enqueued on `stream`.
+int synth_kdk_step(double *x, double *y, double *z, double *vx, double *vy, double *vz, int64_t n, int64_t start,
                    double central_mass, double eps2, double dt, void *stream) {
     if (n <= 0) return 0;
     int dev = 0, sms = 148;
@@ -57,7 +57,7 @@ int synth_kdk_step(double *x, double *y, double *z, double *vx, double *vy, doub
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     int64_t blocks = (n + 255) / 256;
     if (blocks > (int64_t)sms * 8) blocks = (int64_t)sms * 8;
-    syn_kdk_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(x, y, z, vx, vy, vz, n, central_mass, eps2, dt);
+    syn_kdk_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(x, y, z, vx, vy, vz, n, start, central_mass, eps2, dt);
     return (int)cudaGetLastError();
 }
 

@@ -135,7 +135,7 @@ def run_fanin(n, steps, res=(512, 512), lo=(-1.0, -1.0), hi=(1.0, 1.0), seed=5, 
                 cols[c] = t
             torch.cuda.synchronize(dev)
         arrs = [db.wrap_tensor(cols[c], stream=S.cuda_stream, mode=db.BIN_ASYNC) for c in ("x", "y", "mass")]
-        prods.append(dict(dev=dev, S=S, cols=cols, n=r1 - r0, arrs=arrs,
+        prods.append(dict(dev=dev, S=S, cols=cols, n=r1 - r0, r0=r0, arrs=arrs,
                           ptrs=[cols[c].data_ptr() for c in ("x", "y", "z", "vx", "vy", "vz")], ev=[]))
     spec = db.make_spec(res, lo, hi, nattr=1)
     h = db.bin_init(spec, db.make_placement(device_id=0, exec=db.BIN_EXEC_PEER))
@@ -150,7 +150,7 @@ def run_fanin(n, steps, res=(512, 512), lo=(-1.0, -1.0), hi=(1.0, 1.0), seed=5, 
             with torch.cuda.device(q["dev"]):
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(q["S"])
-                synth.kdk_step(q["ptrs"], q["n"], q["S"].cuda_stream, dt=dt)
+                synth.kdk_step(q["ptrs"], q["n"], q["S"].cuda_stream, dt=dt, start=q["r0"])
                 e1.record(q["S"])
                 q["ev"].append((e0, e1))
         ticket = db.bin_execute_shards(h, shards)
