@@ -362,6 +362,11 @@ int bin_multi_execute(bin_multi_t *m, bin_array_t *const *cols, int32_t ncols, u
  * instance saw no finite rows. */
 int bin_multi_wait(bin_multi_t *m, uint64_t ticket);
 
+/* Event after which the producer may overwrite the columns of `ticket`
+ * (their snapshot/staging copies done, or the accumulate done when read in
+ * place); as bin_inputs_released. */
+int bin_multi_inputs_released(bin_multi_t *m, uint64_t ticket, bin_event_t *ev);
+
 /* Waits, then fills *out with instance `op`'s result (library-owned device
  * pointers, same layout and sentinels as bin_result).  BIN_EINVAL for op out
  * of range. */

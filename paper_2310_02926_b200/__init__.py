@@ -249,6 +249,12 @@ def bin_multi_execute(m, cols):
     return t.value
 
 
+def bin_multi_inputs_released(m, ticket):
+    ev = ctypes.c_void_p()
+    check(_lib.bin_multi_inputs_released(ctypes.c_void_p(m), ticket, ctypes.byref(ev)), "bin_multi_inputs_released")
+    return ev.value
+
+
 def bin_multi_wait(m, ticket):
     check(_lib.bin_multi_wait(ctypes.c_void_p(m), ticket), "bin_multi_wait")
 

@@ -111,6 +111,7 @@ _SIGS = {
                                       _P(bin_comm_t), _P(_vp)]),
     "bin_multi_execute": (ctypes.c_int, [_vp, _P(_vp), ctypes.c_int32, _P(ctypes.c_uint64)]),
     "bin_multi_wait": (ctypes.c_int, [_vp, ctypes.c_uint64]),
+    "bin_multi_inputs_released": (ctypes.c_int, [_vp, ctypes.c_uint64, _P(_vp)]),
     "bin_multi_result": (ctypes.c_int, [_vp, ctypes.c_uint64, ctypes.c_int32, _P(bin_result_t)]),
     "bin_multi_profile_enable": (ctypes.c_int, [_vp, ctypes.c_int32]),
     "bin_multi_profile_read": (ctypes.c_int, [_vp, _P(bin_profile_t)]),

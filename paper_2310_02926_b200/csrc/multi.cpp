@@ -373,10 +373,6 @@ int bin_multi_execute(bin_multi_t *m, bin_array_t *const *cols, int32_t ncols, u
     S.launches = 0;
     m->last = s;
     for (bool &r : S.recd) r = false;
-    if (m->prof) {
-        DB_CUDA(cudaEventRecord(S.ev[MEV_START], s));
-        S.recd[MEV_START] = true;
-    }
     // ---- a1: view resolution (zero copy on the analysis device, else staged)
     MultiArgs a{};
     a.n = n;
@@ -452,7 +448,10 @@ int bin_multi_execute(bin_multi_t *m, bin_array_t *const *cols, int32_t ncols, u
         }
         return BIN_OK;
     };
+    // profiled phases start once the inputs are ready (after the producer /
+    // staging waits): the phase times are the analysis' own device time
     int rc;
+    if ((rc = rec(MEV_START, true))) return rc;
     cudaError_t e;
     // ---- a3 for all K
     if ((e = launch_multi_init(a, m->max_work, s)) != cudaSuccess) return cuda_error(e, "multi init kernel");
@@ -538,6 +537,14 @@ static void m_accumulate_profile(bin_multi *m, MSlot &S) {
     p.kernel_launches += S.launches;
     p.bin_launches += 1;
     p.variant = S.variant;
+}
+
+int bin_multi_inputs_released(bin_multi_t *m, uint64_t ticket, bin_event_t *ev) {
+    if (!m || !ev) return set_error(BIN_EINVAL, "bin_multi_inputs_released: NULL argument");
+    MSlot *S = m_find(m, ticket);
+    if (!S) return set_error(BIN_ESTATE, "unknown or recycled ticket %llu", (unsigned long long)ticket);
+    *ev = (bin_event_t)S->released;
+    return BIN_OK;
 }
 
 int bin_multi_wait(bin_multi_t *m, uint64_t ticket) {

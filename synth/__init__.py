@@ -54,6 +54,8 @@ def _load():
                                               ctypes.c_uint64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]
             lib.synth_kdk_step.argtypes = [ctypes.c_void_p] * 6 + [ctypes.c_int64, ctypes.c_int64, ctypes.c_double,
                                                                    ctypes.c_double, ctypes.c_double, ctypes.c_void_p]
+            lib.synth_direct_step.argtypes = [ctypes.c_void_p] * 7 + [ctypes.c_int64, ctypes.c_double, ctypes.c_double,
+                                                                      ctypes.c_void_p]
             _lib = lib
     return _lib
 
@@ -79,6 +81,14 @@ def kdk_step(cols, n, stream=0, central_mass=1000.0, eps2=1e-4, dt=1e-5, start=0
                                 ctypes.c_void_p(stream))
     if rc != 0:
         raise RuntimeError(f"synth_kdk_step: cudaError {rc}")
+
+
+def direct_step(cols, n, stream=0, eps2=1e-4, dt=1e-6):
+    """One O(N^2) direct-sum gravity step (the Newton++ solver class) on device
+    columns (x, y, z, vx, vy, vz, mass as device pointers); synth.cu."""
+    rc = _load().synth_direct_step(*[ctypes.c_void_p(c) for c in cols], int(n), eps2, dt, ctypes.c_void_p(stream))
+    if rc != 0:
+        raise RuntimeError(f"synth_direct_step: cudaError {rc}")
 
 
 # ---------------------------------------------------------------- numpy twin

@@ -46,7 +46,68 @@ __global__ void syn_kdk_kernel(double *x, double *y, double *z, double *vx, doub
     }
 }
 
+// Direct-sum gravity (the Newton++ solver class): every body
+// feels every other body (softened, G = 1).  One symplectic-Euler step: the
+// velocity kick from the O(N^2) force, then the drift (separate kernel, so no
+// position is overwritten while another thread still reads it).  Tiles of
+// DS_TILE bodies are staged in shared memory; j runs in the same order for
+// every i and every launch, so trajectories are reproducible bit for bit.
+constexpr int DS_TILE = 256;
+__global__ void __launch_bounds__(DS_TILE) syn_direct_kick(const double *x, const double *y, const double *z,
+                                                           double *vx, double *vy, double *vz, const double *m,
+                                                           int64_t n, double eps2, double dt) {
+    __shared__ double sx[DS_TILE], sy[DS_TILE], sz[DS_TILE], sm[DS_TILE];
+    const int64_t i = (int64_t)blockIdx.x * DS_TILE + threadIdx.x;
+    const double px = i < n ? x[i] : 0.0, py = i < n ? y[i] : 0.0, pz = i < n ? z[i] : 0.0;
+    double ax = 0.0, ay = 0.0, az = 0.0;
+    for (int64_t j0 = 0; j0 < n; j0 += DS_TILE) {
+        const int64_t j = j0 + threadIdx.x;
+        __syncthreads();
+        sx[threadIdx.x] = j < n ? x[j] : 0.0;
+        sy[threadIdx.x] = j < n ? y[j] : 0.0;
+        sz[threadIdx.x] = j < n ? z[j] : 0.0;
+        sm[threadIdx.x] = j < n ? m[j] : 0.0;
+        __syncthreads();
+        const int cnt = (int)(n - j0 < DS_TILE ? n - j0 : DS_TILE);
+#pragma unroll 8
+        for (int k = 0; k < cnt; ++k) {
+            const double dx = sx[k] - px, dy = sy[k] - py, dz = sz[k] - pz;
+            const double r2 = fma(dx, dx, fma(dy, dy, fma(dz, dz, eps2)));
+            const double ri = rsqrt(r2);
+            const double f = sm[k] * ri * ri * ri;  // the self term has dx = dy = dz = 0
+            ax = fma(f, dx, ax);
+            ay = fma(f, dy, ay);
+            az = fma(f, dz, az);
+        }
+    }
+    if (i < n) {
+        vx[i] += dt * ax;
+        vy[i] += dt * ay;
+        vz[i] += dt * az;
+    }
+}
+__global__ void syn_drift(double *x, double *y, double *z, const double *vx, const double *vy, const double *vz,
+                          int64_t n, double dt) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        x[i] += dt * vx[i];
+        y[i] += dt * vy[i];
+        z[i] += dt * vz[i];
+    }
+}
+
 extern "C" {
+
+// One direct-sum step of n bodies (device columns x y z vx vy vz m), on `stream`.
+int synth_direct_step(double *x, double *y, double *z, double *vx, double *vy, double *vz, const double *m,
+                      int64_t n, double eps2, double dt, void *stream) {
+    if (n <= 0) return 0;
+    const unsigned blocks = (unsigned)((n + DS_TILE - 1) / DS_TILE);
+    syn_direct_kick<<<blocks, DS_TILE, 0, (cudaStream_t)stream>>>(x, y, z, vx, vy, vz, m, n, eps2, dt);
+    syn_drift<<<(unsigned)((n + 255) / 256 < 148 * 8 ? (n + 255) / 256 : 148 * 8), 256, 0, (cudaStream_t)stream>>>(
+        x, y, z, vx, vy, vz, n, dt);
+    return (int)cudaGetLastError();
+}
 
 // One KDK step of n bodies (device columns; row 0 is global row `start`), enqueued on `stream`.
 int synth_kdk_step(double *x, double *y, double *z, double *vx, double *vy, double *vz, int64_t n, int64_t start,

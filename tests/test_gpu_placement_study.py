@@ -19,3 +19,13 @@ def test_placement_modes_agree_and_do_not_interfere(cuda_available):
     assert ps.check(results)
     for m, _, _ in results:
         assert m["solver_ms_per_step"] > 0 and m["actual_insitu_ms_per_step"] > 0
+
+
+def test_direct_sum_study_modes_agree(cuda_available):
+    """Compute-bound producer (O(N^2) direct sum) + the fused paper step, lockstep
+    and asynchronous: identical trajectories, grids equal to the oracle."""
+    if not cuda_available:
+        pytest.fail("needs a CUDA device")
+    from tools import insitu_direct_study as ds
+    results = [ds.run(m, 4099, 4) for m in ("lockstep", "async_snapshot", "async_inplace")]
+    assert ds.check(results)
