@@ -65,7 +65,7 @@ struct FastCtx {
     uint32_t sb;           // shared-window address of f_dsm[0]
 };
 
-template <int D, int A, int SM, int MM>
+template <int D, int A, int SM, int MM, bool XS>
 __device__ __forceinline__ uint32_t fast_row(const FastCtx<D> &c, const double (&x)[D], double v, bool valid,
                                              uint32_t &n_in) {
     constexpr bool HS = A == 1 && SM == 1, HM = A == 1 && MM == 1;
@@ -97,8 +97,15 @@ __device__ __forceinline__ uint32_t fast_row(const FastCtx<D> &c, const double (
     if (HS) {
         const uint32_t w0 = c.o_fx + l;
         unsigned qmid;
-        if (fx_path(c.fx, v)) {
-            const unsigned long long q = fx_quant(c.fx, v);
+        unsigned long long q = 0;
+        bool fx;
+        if (XS) {
+            fx = fx_quant_exact(c.fx, v, q);
+        } else {
+            fx = fx_path(c.fx, v);
+            if (fx) q = fx_quant(c.fx, v);
+        }
+        if (fx) {
             const unsigned qlo = (unsigned)q;
             qmid = (unsigned)(q >> 32);
             const unsigned old = BIN_SADDR ? s_atom_add(c.sb + 4u * w0, qlo) : atomicAdd(&f_dsm[w0], qlo);
@@ -348,7 +355,7 @@ __global__ void __launch_bounds__(FAST_THREADS, 1)
             acc.window[3 + d] = d < D ? (int)c.we[d < D ? d : 0] : 1;
         }
     }
-    c.fx = fx_param(HS ? s_exp : 0u);
+    c.fx = XS ? fx_param_exact(s_exp) : fx_param(HS ? s_exp : 0u);
 #ifdef BIN_GF_OFF
     const bool gf = false;
 #else
@@ -392,11 +399,11 @@ __global__ void __launch_bounds__(FAST_THREADS, 1)
         double x[D];
 #pragma unroll
         for (int d = 0; d < D; ++d) x[d] = bx[d].x;
-        uint32_t t0 = fast_row<D, A, SM, MM>(c, x, bv.x, valid, n_in);
+        uint32_t t0 = fast_row<D, A, SM, MM, XS>(c, x, bv.x, valid, n_in);
         fast_push<A, SM, MM, XS>(qb, qn, t0, bv.x, lane, count, sum, mm, gf, X);
 #pragma unroll
         for (int d = 0; d < D; ++d) x[d] = bx[d].y;
-        uint32_t t1 = fast_row<D, A, SM, MM>(c, x, bv.y, valid, n_in);
+        uint32_t t1 = fast_row<D, A, SM, MM, XS>(c, x, bv.y, valid, n_in);
         fast_push<A, SM, MM, XS>(qb, qn, t1, bv.y, lane, count, sum, mm, gf, X);
         rows += valid ? 2u : 0u;
 #pragma unroll
@@ -411,7 +418,7 @@ __global__ void __launch_bounds__(FAST_THREADS, 1)
 #pragma unroll
         for (int d = 0; d < D; ++d) x[d] = r >= 0 ? in.ax[d][r] : 0.0;
         if (A == 1 && r >= 0) v = in.at[0][r];
-        const uint32_t t = fast_row<D, A, SM, MM>(c, x, v, r >= 0, n_in);
+        const uint32_t t = fast_row<D, A, SM, MM, XS>(c, x, v, r >= 0, n_in);
         rows += r >= 0 ? 1u : 0u;
         fast_push<A, SM, MM, XS>(qb, qn, t, v, lane, count, sum, mm, gf, X);
     }

@@ -85,8 +85,15 @@ __device__ __forceinline__ void accumulate_row(const GenCtx &c, const FxParam (&
                 const uint32_t s = __popc(c.sum_mask & ((1u << a) - 1u));
                 const uint32_t w0 = c.o_fx + s * 3 * W + l;
                 unsigned qmid;
-                if (fx_path(fx[a], v[a])) {
-                    const unsigned long long q = fx_quant(fx[a], v[a]);
+                unsigned long long q = 0;
+                bool fxp;
+                if (c.xs) {
+                    fxp = fx_quant_exact(fx[a], v[a], q);
+                } else {
+                    fxp = fx_path(fx[a], v[a]);
+                    if (fxp) q = fx_quant(fx[a], v[a]);
+                }
+                if (fxp) {
                     const unsigned qlo = (unsigned)q;
                     qmid = (unsigned)(q >> 32);
                     const unsigned old = atomicAdd(&g_dsm[w0], qlo);
@@ -165,7 +172,7 @@ __global__ void __launch_bounds__(GenThreads<A>::value, 1)
     constexpr int AA = A > 0 ? A : 1;
     FxParam fx[AA];
 #pragma unroll
-    for (int a = 0; a < A; ++a) fx[a] = fx_param(acc.fxexp[a]);
+    for (int a = 0; a < A; ++a) fx[a] = acc.xs ? fx_param_exact(acc.fxexp[a]) : fx_param(acc.fxexp[a]);
     const uint32_t load_mask = acc.load_mask;
 
     for (uint32_t i = threadIdx.x; i < c.o_fx; i += blockDim.x) g_dsm[i] = ~0u;  // filters

@@ -572,6 +572,13 @@ __global__ void __launch_bounds__(PART_THREADS, 1) k_part_reduce(Accum acc, Part
             for (int w = 0; w < PART_THREADS / 32; ++w) best = max(best, s_best[j][w]);
             // exponents [e, e + 9) -> fx_param(fxexp = e + 6) (eb_hi = fxexp + 3)
             fx[j] = fx_param(best ? (best & 2047u) + 6u : 0u);
+            if (acc.xs) {  // exact sums: grid topped by the window's highest sampled binade
+                unsigned top = 0;
+                if (best)
+                    for (unsigned k = 0; k < 9; ++k)
+                        if (eh[j * 2048 + (best & 2047u) + k]) top = (best & 2047u) + k;
+                fx[j] = fx_param_exact(top);
+            }
         }
         __syncthreads();
     }
@@ -630,8 +637,15 @@ __global__ void __launch_bounds__(PART_THREADS, 1) k_part_reduce(Accum acc, Part
                     if (ss[j] >= 0) {
                         const uint32_t w0 = o_fx + (uint32_t)ss[j] * 3u * W + l;
                         unsigned qmid;
-                        if (fx_path(fx[j], x)) {
-                            const unsigned long long q = fx_quant(fx[j], x);
+                        unsigned long long q = 0;
+                        bool fxp;
+                        if (acc.xs) {
+                            fxp = fx_quant_exact(fx[j], x, q);
+                        } else {
+                            fxp = fx_path(fx[j], x);
+                            if (fxp) q = fx_quant(fx[j], x);
+                        }
+                        if (fxp) {
                             const unsigned qlo = (unsigned)q;
                             qmid = (unsigned)(q >> 32);
                             const unsigned old = atomicAdd(&p_dsm[w0], qlo);

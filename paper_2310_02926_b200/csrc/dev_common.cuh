@@ -90,11 +90,14 @@ __device__ __forceinline__ bool bin_coords(const DGeom &G, const double (&x)[D],
 }
 
 // ---- fixed-point window sums (see bin_general.cu / bin_fast.cu headers) ----
-// q' = round(v * 2^F) + 2^62 with |round(v * 2^F)| < 2^62, summed exactly in
-// 96 bits; the flush subtracts count * 2^62.  (The count cannot be recovered
-// from the sum alone: sum q / 2^63 is not bounded by 1/2 -- tried and
+// q' = round(v * 2^F) + 2^54 with |round(v * 2^F)| < 2^54, summed exactly in
+// 96 bits; the flush subtracts count * 2^54.  (The count cannot be recovered
+// from the sum alone: sum q / 2^55 is not bounded by 1/2 -- tried and
 // rejected, WE4 catches it -- so windows keep an explicit count.)
-constexpr long long FX_OFFSET = 1ll << 62;
+// |q| < 2^54 keeps the middle word's per-row addend below 2^23, so it carries
+// into the high word only every ~500 rows (a wider q made every ~4th row pay
+// an extra shared atomic: +3.1M ATOMS on C3).
+constexpr long long FX_OFFSET = 1ll << 54;
 constexpr unsigned FX_OFFSET_MID = (unsigned)(FX_OFFSET >> 32);
 
 struct FxParam {
@@ -105,14 +108,13 @@ struct FxParam {
     unsigned span;
 };
 
-// F from the sampled max exponent of the attribute: E_hi = e_max + 3 (biased
-// eb_hi), F = 62 - E_hi; values in [2^(E_hi-9), 2^E_hi) have their last
-// mantissa bit at or above 2^(E_hi-61) >= 2^-F, so round(v * 2^F) is exact:
-// the window sums are exact integers (|q| < 2^62, 96 bits hold 2^33 of them).
+// BIN_SUM_FAST: F from the sampled max exponent of the attribute: E_hi = e_max
+// + 3 (biased eb_hi), F = 54 - E_hi; values in [2^(E_hi-9), 2^E_hi) ->
+// quantisation <= 2^-46 |v| (within reading R8).
 __device__ __forceinline__ FxParam fx_param(unsigned fxexp) {
     int eb_hi = (int)fxexp + 3;
     if (fxexp == 0) eb_hi = 1023 + 1;  // nothing sampled: assume |v| < 2
-    const int F = 62 - (eb_hi - 1023);
+    const int F = 54 - (eb_hi - 1023);
     const bool usable = F > -900 && F < 900;
     const int eb_lo = max(eb_hi - 9, 1);
     FxParam P;
@@ -124,14 +126,34 @@ __device__ __forceinline__ FxParam fx_param(unsigned fxexp) {
     return P;
 }
 
+// BIN_SUM_EXACT: the grid's top binade is the sampled max one (E_hi = e_max
+// + 1, F = 54 - E_hi), so every value of that binade and the next lies on the
+// grid 2^-F exactly; a value takes the fixed path only if it is exactly on
+// the grid and |q| < 2^54 (fx_quant_exact), else it goes to the digit rows.
+__device__ __forceinline__ FxParam fx_param_exact(unsigned fxexp) {
+    FxParam P = fx_param(fxexp == 0 ? 0u : (fxexp < 3u ? 1u : fxexp - 2u));
+    P.lo = 1u;  // the exactness test decides
+    P.span = P.scale != 0.0 ? 2046u : 0u;
+    return P;
+}
+
 __device__ __forceinline__ bool fx_path(const FxParam &P, double v) {
     const unsigned eb = ((unsigned)__double2hiint(v) >> 20) & 0x7ffu;
     return eb - P.lo < P.span || v == 0.0;
 }
 
-// q' = round(v * 2^F) + 2^62 in (0, 2^63)
+// q' = round(v * 2^F) + 2^54 in (0, 2^55)
 __device__ __forceinline__ unsigned long long fx_quant(const FxParam &P, double v) {
     return (unsigned long long)(__double2ll_rn(__dmul_rn(v, P.scale)) + FX_OFFSET);
+}
+
+// exact mode: q' as above when v * 2^F is an integer below 2^54 in magnitude
+// (the multiply by a power of two is exact unless it leaves the normal range,
+// which the round trip q * 2^-F == v also rules out); false -> digit rows.
+__device__ __forceinline__ bool fx_quant_exact(const FxParam &P, double v, unsigned long long &qp) {
+    const long long q = __double2ll_rn(__dmul_rn(v, P.scale));
+    qp = (unsigned long long)(q + FX_OFFSET);
+    return P.span != 0u && q > -FX_OFFSET && q < FX_OFFSET && __dmul_rn(__ll2double_rn(q), P.inv_scale) == v;
 }
 
 // Exact 96-bit fixed-point sum of cnt offset values -> f64 (one rounding when
