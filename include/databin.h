@@ -325,7 +325,8 @@ const char *bin_version(void);
  * readings R1-R17; counts/min/max bit-identical, sums within reading R8).
  *
  * bin_multi_op_t: spec = the instance's mesh, bounds and reductions
- *   (deterministic must be 0 -> else BIN_ENOTSUP; route is ignored);
+ *   (deterministic must be 0 -> else BIN_ENOTSUP; route is ignored;
+ *   sum_mode BIN_SUM_EXACT gives that instance once-rounded exact sums);
  *   axis_col[d] / attr_col[a] = indices into the column list given to
  *   bin_multi_execute (0 <= index < ncols; a column may serve any number of
  *   instances, as axis or attribute).

@@ -30,7 +30,9 @@ struct MSlot {
     double *sum = nullptr;
     unsigned long long *mm = nullptr;
     unsigned long long *bounds = nullptr;
-    uint64_t n_count = 0, n_sum = 0, n_mm = 0, n_bounds = 0;
+    long long *xs = nullptr;      // exact-sum digits of all exact instances (type-major)
+    int32_t *xrange = nullptr;    // 2 * BIN_MAX_ATTR per instance
+    uint64_t n_count = 0, n_sum = 0, n_mm = 0, n_bounds = 0, n_xs = 0;
     Meta *meta_d = nullptr;            // [K]
     Meta *meta_h = nullptr;            // pinned mirror
     bool meta_valid = false;
@@ -81,7 +83,7 @@ static int alloc_mslot(bin_multi *m, MSlot &S) {
     const int K = m->K;
     std::vector<uint64_t> B(K);
     std::vector<int> ns(K), nm(K);
-    uint64_t nc = 0, nsu = 0, nmm = 0, nout_mm = 0, nout_avg = 0;
+    uint64_t nc = 0, nsu = 0, nmm = 0, nout_mm = 0, nout_avg = 0, nxs = 0;
     for (int k = 0; k < K; ++k) {
         const bin_spec_t &sp = m->ops[k].spec;
         uint64_t b = 1;
@@ -92,6 +94,7 @@ static int alloc_mslot(bin_multi *m, MSlot &S) {
             if (sp.ops[a] & (BIN_OP_SUM | BIN_OP_AVG)) ns[k]++;
             if (sp.ops[a] & (BIN_OP_MIN | BIN_OP_MAX)) nm[k]++;
         }
+        if (sp.sum_mode == BIN_SUM_EXACT) nxs += b * ns[k] * XD_DIGITS;
         nc += b + 2;
         nsu += b * ns[k];
         nmm += 2 * b * nm[k];
@@ -109,6 +112,8 @@ static int alloc_mslot(bin_multi *m, MSlot &S) {
     const size_t o_meta = o; o += al((size_t)K * sizeof(Meta));
     const size_t o_ops = o; o += al((size_t)K * sizeof(MultiOp));
     const size_t o_scratch = o; o += al(256);
+    const size_t o_xrange = o; o += al((size_t)K * 2 * BIN_MAX_ATTR * 4);
+    const size_t o_xs = o; o += al(nxs * 8);
     const size_t total = o;
     cudaError_t e = cudaMalloc(&S.base, total);
     if (e != cudaSuccess) {
@@ -125,10 +130,14 @@ static int alloc_mslot(bin_multi *m, MSlot &S) {
     S.mm = (unsigned long long *)(b0 + o_mm);
     S.bounds = (unsigned long long *)(b0 + o_bounds);
     S.n_count = nc, S.n_sum = nsu, S.n_mm = nmm, S.n_bounds = (uint64_t)K * 6;
+    S.xrange = (int32_t *)(b0 + o_xrange);
+    S.xs = nxs ? (long long *)(b0 + o_xs) : nullptr;
+    S.n_xs = nxs;
+    DB_CUDA(cudaMemset(S.xrange, 0x7f, (size_t)K * 2 * BIN_MAX_ATTR * 4));
     S.meta_d = (Meta *)(b0 + o_meta);
     S.ops_d = (MultiOp *)(b0 + o_ops);
     S.ops_h.assign(K, MultiOp{});
-    uint64_t pc = 0, ps = 0, pm = 0, pomm = 0, poavg = 0;
+    uint64_t pc = 0, ps = 0, pm = 0, pomm = 0, poavg = 0, px = 0;
     for (int k = 0; k < K; ++k) {
         const bin_multi_op_t &op = m->ops[k];
         MultiOp &t = S.ops_h[k];
@@ -160,6 +169,11 @@ static int alloc_mslot(bin_multi *m, MSlot &S) {
             if (op.spec.ops[a] & (BIN_OP_MIN | BIN_OP_MAX)) acc.mm_mask |= 1u << a;
         }
         acc.load_mask = acc.sum_mask | acc.mm_mask;
+        if (op.spec.sum_mode == BIN_SUM_EXACT && ns[k] > 0) {
+            acc.xs = S.xs + px;
+            acc.xrange = S.xrange + (size_t)k * 2 * BIN_MAX_ATTR;
+            px += B[k] * ns[k] * XD_DIGITS;
+        }
         t.meta = S.meta_d + k;
         pc += B[k] + 2;
         ps += B[k] * ns[k];
@@ -216,8 +230,6 @@ int bin_multi_init(const bin_multi_op_t *ops, int32_t nops, int32_t ncols, const
             const std::string msg = bin_last_error();
             return set_error(rc, "instance %d: %s", k, msg.c_str());
         }
-        if (ops[k].spec.sum_mode == BIN_SUM_EXACT)
-            return set_error(BIN_ENOTSUP, "instance %d: BIN_SUM_EXACT is not fused (use bin_init)", k);
         if (ops[k].spec.deterministic)
             return set_error(BIN_ENOTSUP, "instance %d: deterministic mode is not fused (use bin_init)", k);
         int ns = 0, nm = 0;
@@ -456,6 +468,11 @@ int bin_multi_execute(bin_multi_t *m, bin_array_t *const *cols, int32_t ncols, u
     // ---- a3 for all K
     if ((e = launch_multi_init(a, m->max_work, s)) != cudaSuccess) return cuda_error(e, "multi init kernel");
     S.launches++;
+    if (S.xs) {  // exact sums: digits cleared; reset every instance's touched range
+        if (n >= (1ll << 30))
+            return set_error(BIN_EINVAL, "BIN_SUM_EXACT: %lld rows per execute (limit 2^30)", (long long)n);
+        DB_CUDA(cudaMemsetAsync(S.xrange, 0x7f, (size_t)m->K * 2 * BIN_MAX_ATTR * 4, s));
+    }
     if ((rc = rec(MEV_INIT, true))) return rc;
     // ---- a2 for every auto-bounded axis column (+ cross-rank Min)
     if (m->bound_cols) {
@@ -481,6 +498,11 @@ int bin_multi_execute(bin_multi_t *m, bin_array_t *const *cols, int32_t ncols, u
         if (r == ncclSuccess) r = ncclAllReduce(S.count, S.count, S.n_count, ncclUint64, ncclSum, m->comm, s);
         if (r == ncclSuccess && S.n_sum) r = ncclAllReduce(S.sum, S.sum, S.n_sum, ncclFloat64, ncclSum, m->comm, s);
         if (r == ncclSuccess && S.n_mm) r = ncclAllReduce(S.mm, S.mm, S.n_mm, ncclUint64, ncclMin, m->comm, s);
+        if (r == ncclSuccess && S.n_xs) {  // exact sums: integer digits add exactly; ranges unite
+            r = ncclAllReduce(S.xs, S.xs, S.n_xs, ncclInt64, ncclSum, m->comm, s);
+            if (r == ncclSuccess)
+                r = ncclAllReduce(S.xrange, S.xrange, (size_t)m->K * 2 * BIN_MAX_ATTR, ncclInt32, ncclMin, m->comm, s);
+        }
         ncclResult_t r2 = ncclGroupEnd();
         if (r != ncclSuccess) return m_nccl_error(r, "ncclAllReduce(multi bins)");
         if (r2 != ncclSuccess) return m_nccl_error(r2, "ncclGroupEnd");

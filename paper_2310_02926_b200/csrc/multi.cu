@@ -25,6 +25,7 @@
 #include "db_internal.h"
 #include "dev_common.cuh"
 #include "tail.cuh"
+#include "xsum.cuh"
 
 namespace db {
 
@@ -43,6 +44,15 @@ __global__ void __launch_bounds__(MULTI_INIT_THREADS) k_multi_init(MultiArgs a) 
     const ulonglong2 ident = make_ulonglong2(~0ull, ~0ull);
     for (int64_t i = t0; i < (int64_t)(nb * acc.nmm); i += stride) ((ulonglong2 *)acc.mm)[i] = ident;
     if (t0 < 2 * o.g.ndim) acc.bounds[t0] = ~0ull;
+    if (acc.xs) {  // exact sums: clear the digits of the slot's previous execute (range reset after)
+        for (int s = 0; s < acc.nsum; ++s) {
+            const int klo = acc.xrange[2 * s], khi = -acc.xrange[2 * s + 1];
+            if (klo == XR_EMPTY || klo > khi) continue;
+            long long *d = acc.xs + ((uint64_t)s * XD + klo) * nb;
+            const int64_t m = (int64_t)(khi - klo + 1) * (int64_t)nb;
+            for (int64_t i = t0; i < m; i += stride) d[i] = 0ll;
+        }
+    }
 }
 
 cudaError_t launch_multi_init(const MultiArgs &a, uint64_t max_work, cudaStream_t s) {
@@ -136,6 +146,8 @@ struct MOpS {
     unsigned long long *count;
     double *sum;
     ulonglong2 *mm;
+    long long *xs;     // BIN_SUM_EXACT digit rows (nullptr: fast sums)
+    int32_t *xrange;
     uint64_t nbins;
     int32_t res[3];
     int32_t axc[3];
@@ -148,6 +160,7 @@ __global__ void __launch_bounds__(MULTI_THREADS) k_multi_bin(MultiArgs a) {
     __shared__ MOpS so[MULTI_MAX_OPS];
     __shared__ double sv[MULTI_MAX_COLS][MULTI_THREADS];  // this CTA's rows, one column per line
     __shared__ unsigned s_in[MULTI_MAX_OPS], s_out[MULTI_MAX_OPS];
+    __shared__ int s_xr[MULTI_MAX_OPS][2 * BIN_MAX_ATTR];  // exact sums: digits touched per instance
     const int K = a.k1 - a.k0;  // this launch's group of instances
     if (threadIdx.x < K) {
         const MultiOp &o = a.ops[a.k0 + threadIdx.x];
@@ -164,6 +177,8 @@ __global__ void __launch_bounds__(MULTI_THREADS) k_multi_bin(MultiArgs a) {
         t.count = o.acc.count;
         t.sum = o.acc.sum;
         t.mm = (ulonglong2 *)o.acc.mm;
+        t.xs = o.acc.xs;
+        t.xrange = o.acc.xrange;
         t.nbins = o.acc.nbins;
         t.ndim = o.g.ndim;
         t.nattr = o.nattr;
@@ -176,6 +191,7 @@ __global__ void __launch_bounds__(MULTI_THREADS) k_multi_bin(MultiArgs a) {
         s_in[threadIdx.x] = 0u;
         s_out[threadIdx.x] = 0u;
     }
+    for (int i = threadIdx.x; i < MULTI_MAX_OPS * 2 * BIN_MAX_ATTR; i += MULTI_THREADS) (&s_xr[0][0])[i] = XR_EMPTY;
     __syncthreads();
     const unsigned lane = threadIdx.x & 31u;
     const int64_t stride = (int64_t)gridDim.x * MULTI_THREADS;
@@ -211,7 +227,10 @@ __global__ void __launch_bounds__(MULTI_THREADS) k_multi_bin(MultiArgs a) {
             // serialises behind the preceding reductions: slower here)
             for (int j = 0; j < o.nattr; ++j) {
                 const double v = sv[o.atc[j]][threadIdx.x];
-                if (o.sslot[j] >= 0) red_add_f64(&o.sum[(uint64_t)o.sslot[j] * B + b], v);
+                if (o.sslot[j] >= 0) {
+                    if (o.xs) xsum_add_double(o.xs, B, o.sslot[j], b, v, s_xr[k]);
+                    else red_add_f64(&o.sum[(uint64_t)o.sslot[j] * B + b], v);
+                }
                 if (o.mslot[j] >= 0) {
                     ulonglong2 *p = o.mm + (uint64_t)o.mslot[j] * B + b;
                     const unsigned long long e = enc_total(v);
@@ -226,6 +245,10 @@ __global__ void __launch_bounds__(MULTI_THREADS) k_multi_bin(MultiArgs a) {
         const MOpS &o = so[threadIdx.x];
         if (s_in[threadIdx.x]) red_add_u64(&o.count[o.nbins], (unsigned long long)s_in[threadIdx.x]);
         if (s_out[threadIdx.x]) red_add_u64(&o.count[o.nbins + 1], (unsigned long long)s_out[threadIdx.x]);
+    }
+    for (int i = threadIdx.x; i < K * 2 * BIN_MAX_ATTR; i += MULTI_THREADS) {  // publish the digit ranges
+        const int k = i / (2 * BIN_MAX_ATTR), t = i % (2 * BIN_MAX_ATTR);
+        if (so[k].xs && s_xr[k][t] != XR_EMPTY) atomicMin(&so[k].xrange[t], s_xr[k][t]);
     }
 }
 

@@ -157,6 +157,46 @@ def test_multi_matches_separate_instances(db):
 
 
 @pytest.mark.gpu
+def test_multi_exact_instances(db):
+    """BIN_SUM_EXACT instances inside a fused set: sums bit-exact vs the oracle's exact sums."""
+    rng = np.random.default_rng(12)
+    n = 250_001
+    cols = [rng.normal(0, 1, n), rng.normal(0, 1, n),
+            rng.normal(0, 1, n) * np.ldexp(1.0, rng.integers(-30, 30, n)), rng.uniform(0.5, 1.5, n)]
+    insts = [dict(res=(40, 30), lo=(-3.0, -3.0), hi=(3.0, 3.0), axes=(0, 1), attrs=(2, 3), exact=True),
+             dict(res=(64,), lo=(-3.0,), hi=(3.0,), axes=(1,), attrs=(2,), exact=False),
+             dict(res=(16, 16), bounds_auto=True, axes=(0, 3), attrs=(2,), exact=True)]
+    import torch
+    dev = torch.device("cuda:0")
+    ts = [torch.from_numpy(c).to(dev) for c in cols]
+    hs = [db.wrap_tensor(t) for t in ts]
+    torch.cuda.synchronize()
+    specs = [db.make_spec(d["res"], d.get("lo"), d.get("hi"), nattr=len(d["attrs"]),
+                          bounds_auto=d.get("bounds_auto", False), exact=d["exact"]) for d in insts]
+    m = db.bin_multi_init([db.make_multi_op(sp, d["axes"], d["attrs"]) for sp, d in zip(specs, insts)], len(cols),
+                          db.make_placement(device_id=0))
+    try:
+        outs = []
+        for _ in range(3):  # repeated executes: digit ranges cleared between them
+            t = db.bin_multi_execute(m, hs)
+            outs.append([db.result_to_numpy(m, t, sp, op=k) for k, sp in enumerate(specs)])
+    finally:
+        db.bin_multi_finalize(m)
+        for a in hs:
+            db.bin_array_release(a)
+    for d, out in zip(insts, outs[-1]):
+        ref = oracle.databin([cols[i] for i in d["axes"]], [cols[i] for i in d["attrs"]], d["res"], d.get("lo"),
+                             d.get("hi"), bounds_auto=d.get("bounds_auto", False), exact=True)
+        compare(out, ref)
+        if d["exact"]:
+            for a in range(len(d["attrs"])):
+                assert np.array_equal(out["sum"][a].view(np.uint64), ref["sum_exact"][a].view(np.uint64))
+    for k in range(len(insts)):
+        assert np.array_equal(outs[0][k]["sum"][0].view(np.uint64), outs[2][k]["sum"][0].view(np.uint64)) \
+            or not insts[k]["exact"]
+
+
+@pytest.mark.gpu
 def test_multi_degenerate_auto_bounds(db):
     cols = [np.full(10, np.nan), np.linspace(0, 1, 10), np.ones(10)]
     insts = [dict(res=(4,), bounds_auto=True, axes=(0,), attrs=(2,)),

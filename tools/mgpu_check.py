@@ -110,7 +110,7 @@ def main():
     insts = [dict(res=(64, 64), lo=(-1.0, -1.0), hi=(1.0, 1.0), axes=sy, attrs=tuple(range(7)), auto=False)
              for sy in systems] + [dict(res=(50,), axes=(3,), attrs=(4, 5), auto=True)]
     specs = [db.make_spec(d["res"], None if d["auto"] else d["lo"], None if d["auto"] else d["hi"],
-                          nattr=len(d["attrs"]), bounds_auto=d["auto"]) for d in insts]
+                          nattr=len(d["attrs"]), bounds_auto=d["auto"], exact=d["auto"]) for d in insts]
     obj = [db.bin_nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     m = db.bin_multi_init([db.make_multi_op(sp, d["axes"], d["attrs"]) for sp, d in zip(specs, insts)], 7,
@@ -123,10 +123,14 @@ def main():
         host = [synth.fill_host(synth.UNIFORM, 1, 6, c, 0, n) for c in range(7)]
         for k, (d, out) in enumerate(zip(insts, outs)):
             ref = oracle.databin([host[i] for i in d["axes"]], [host[i] for i in d["attrs"]], d["res"],
-                                 None if d["auto"] else d["lo"], None if d["auto"] else d["hi"], bounds_auto=d["auto"])
+                                 None if d["auto"] else d["lo"], None if d["auto"] else d["hi"], bounds_auto=d["auto"],
+                                 exact=True)
             status = "ok"
             try:
                 compare(out, ref)
+                if d["auto"]:  # the exact instance: once-rounded exact sums across ranks
+                    for a in range(len(d["attrs"])):
+                        assert np.array_equal(out["sum"][a].view(np.uint64), ref["sum_exact"][a].view(np.uint64))
                 if d["auto"]:
                     assert np.array_equal(out["lo"], ref["lo"]) and np.array_equal(out["hi"], ref["hi"])
             except AssertionError as e:  # noqa: PERF203
