@@ -55,7 +55,7 @@ __device__ __forceinline__ uint64_t global_bin(const GenCtx &c, const int (&k)[D
     return b;
 }
 
-template <int D, int A>
+template <int D, int A, bool XS>
 __device__ __forceinline__ void accumulate_row(const GenCtx &c, const FxParam (&fx)[A > 0 ? A : 1],
                                                const double (&x)[D], const double (&v)[A > 0 ? A : 1],
                                                uint32_t &n_in) {
@@ -87,7 +87,7 @@ __device__ __forceinline__ void accumulate_row(const GenCtx &c, const FxParam (&
                 unsigned qmid;
                 unsigned long long q = 0;
                 bool fxp;
-                if (c.xs) {
+                if (XS) {
                     fxp = fx_quant_exact(fx[a], v[a], q);
                 } else {
                     fxp = fx_path(fx[a], v[a]);
@@ -99,7 +99,7 @@ __device__ __forceinline__ void accumulate_row(const GenCtx &c, const FxParam (&
                     const unsigned old = atomicAdd(&g_dsm[w0], qlo);
                     qmid += (old + qlo < old) ? 1u : 0u;
                 } else {  // rare: outside the fixed range -> f64 L2 reduction, offset only here
-                    if (c.xs) xsum_add_double(c.xs, c.nbins, (int)s, global_bin<D>(c, k), v[a], c.sxr);
+                    if (XS) xsum_add_double(c.xs, c.nbins, (int)s, global_bin<D>(c, k), v[a], c.sxr);
                     else atomicAdd(&c.sum[(uint64_t)s * c.nbins + global_bin<D>(c, k)], v[a]);
                     qmid = FX_OFFSET_MID;
                 }
@@ -133,7 +133,7 @@ __device__ __forceinline__ void accumulate_row(const GenCtx &c, const FxParam (&
         for (int a = 0; a < A; ++a) {
             if ((c.sum_mask >> a) & 1u) {
                 const uint32_t s = __popc(c.sum_mask & ((1u << a) - 1u));
-                if (c.xs) xsum_add_double(c.xs, c.nbins, (int)s, b, v[a], c.sxr);
+                if (XS) xsum_add_double(c.xs, c.nbins, (int)s, b, v[a], c.sxr);
                 else atomicAdd(&c.sum[(uint64_t)s * c.nbins + b], v[a]);
             }
             if ((c.mm_mask >> a) & 1u) {
@@ -149,13 +149,13 @@ __device__ __forceinline__ void accumulate_row(const GenCtx &c, const FxParam (&
 template <int A>
 struct GenThreads { static constexpr int value = A <= 1 ? 1024 : 512; };
 
-template <int D, int A, bool VEC>
+template <int D, int A, bool VEC, bool XS>
 __global__ void __launch_bounds__(GenThreads<A>::value, 1)
     k_bin(Geom g, Inputs in, Accum acc, int64_t head) {
     __shared__ int s_xr[2 * BIN_MAX_ATTR];
-    xr_init(s_xr);
+    if (XS) xr_init(s_xr);
     GenCtx c;
-    c.xs = acc.xs;
+    c.xs = XS ? acc.xs : nullptr;
     c.sxr = s_xr;
     c.G = load_geom<D>(g, acc.bounds);
     if (!c.G.ok) return;  // degenerate auto bounds: finalize reports it
@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(GenThreads<A>::value, 1)
     constexpr int AA = A > 0 ? A : 1;
     FxParam fx[AA];
 #pragma unroll
-    for (int a = 0; a < A; ++a) fx[a] = acc.xs ? fx_param_exact(acc.fxexp[a]) : fx_param(acc.fxexp[a]);
+    for (int a = 0; a < A; ++a) fx[a] = XS ? fx_param_exact(acc.fxexp[a]) : fx_param(acc.fxexp[a]);
     const uint32_t load_mask = acc.load_mask;
 
     for (uint32_t i = threadIdx.x; i < c.o_fx; i += blockDim.x) g_dsm[i] = ~0u;  // filters
@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(GenThreads<A>::value, 1)
         for (int d = 0; d < D; ++d) x[d] = __ldcs(in.ax[d] + r);
 #pragma unroll
         for (int a = 0; a < A; ++a) v[a] = ((load_mask >> a) & 1u) ? __ldcs(in.at[a] + r) : 0.0;
-        accumulate_row<D, A>(c, fx, x, v, n_in);
+        accumulate_row<D, A, XS>(c, fx, x, v, n_in);
         ++rows_mine;
     };
     if (VEC) {
@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(GenThreads<A>::value, 1)
                 for (int d = 0; d < D; ++d) x[d] = h ? cx[d].y : cx[d].x;
 #pragma unroll
                 for (int a = 0; a < A; ++a) v[a] = h ? cv[a].y : cv[a].x;
-                accumulate_row<D, A>(c, fx, x, v, n_in);
+                accumulate_row<D, A, XS>(c, fx, x, v, n_in);
             }
             rows_mine += 2;
 #pragma unroll
@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(GenThreads<A>::value, 1)
             if ((c.sum_mask >> a) & 1u) {
                 const uint32_t s = __popc(c.sum_mask & ((1u << a) - 1u));
                 const uint32_t w0 = c.o_fx + s * 3 * W + l;
-                if (c.xs) {
+                if (XS) {
                     xsum_add_fixed(c.xs, c.nbins, (int)s, b, g_dsm[w0], g_dsm[w0 + W], g_dsm[w0 + 2 * W], cnt,
                                    FX_OFFSET, fx[a].F, s_xr);
                 } else {
@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(GenThreads<A>::value, 1)
             }
         }
     }
-    if (c.xs) {
+    if (XS) {
         __syncthreads();
         xr_publish(s_xr, acc.nsum, acc.xrange);
     }
@@ -293,7 +293,8 @@ static cudaError_t launch_general(const Geom &g, const Inputs &in, const Accum &
     int blocks = lc.sms;  // one persistent CTA per SM: the whole shared memory holds the window
     const int64_t maxb = (in.n + T - 1) / T;
     if (maxb < blocks) blocks = (int)(maxb > 0 ? maxb : 1);
-    auto kern = vec ? k_bin<D, A, true> : k_bin<D, A, false>;
+    auto kern = acc.xs ? (vec ? k_bin<D, A, true, true> : k_bin<D, A, false, true>)
+                       : (vec ? k_bin<D, A, true, false> : k_bin<D, A, false, false>);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     kern<<<blocks, T, smem, s>>>(g, in, acc, vec ? head : 0);

@@ -511,7 +511,7 @@ __global__ void __launch_bounds__(NT, 2) k_part_refine(PartArgs pa) {
 // Window words: mm u64 {enc(min), ~enc(max)} [nmm][W] (exact) | fixed-point
 // sums u32 [nsum][3][W] | count u32 [W].  Before the first tile the same
 // memory holds the exponent histograms [A][2048] of the CTA's sampled values.
-template <int A>
+template <int A, bool XS>
 __global__ void __launch_bounds__(PART_THREADS, 1) k_part_reduce(Accum acc, PartArgs pa) {
     constexpr int AA = A > 0 ? A : 1;
     constexpr int U = A <= 1 ? 4 : 2;  // rows per thread per stage (two stages in flight)
@@ -522,7 +522,7 @@ __global__ void __launch_bounds__(PART_THREADS, 1) k_part_reduce(Accum acc, Part
     const uint32_t hi = (uint32_t)(((uint64_t)ns * (blockIdx.x + 1)) / gridDim.x);
     if (lo >= hi) return;
     __shared__ int s_xr[2 * BIN_MAX_ATTR];  // BIN_SUM_EXACT: digits this CTA touched (xsum.cuh)
-    xr_init(s_xr);
+    if (XS) xr_init(s_xr);
     const int nl = pa.nl;
     const uint32_t sum_mask = acc.sum_mask, mm_mask = acc.mm_mask;
     int ss[AA], ms[AA];  // sum / min-max slot of load slot j, -1 if none
@@ -572,7 +572,7 @@ __global__ void __launch_bounds__(PART_THREADS, 1) k_part_reduce(Accum acc, Part
             for (int w = 0; w < PART_THREADS / 32; ++w) best = max(best, s_best[j][w]);
             // exponents [e, e + 9) -> fx_param(fxexp = e + 6) (eb_hi = fxexp + 3)
             fx[j] = fx_param(best ? (best & 2047u) + 6u : 0u);
-            if (acc.xs) {  // exact sums: grid topped by the window's highest sampled binade
+            if (XS) {  // exact sums: grid topped by the window's highest sampled binade
                 unsigned top = 0;
                 if (best)
                     for (unsigned k = 0; k < 9; ++k)
@@ -639,7 +639,7 @@ __global__ void __launch_bounds__(PART_THREADS, 1) k_part_reduce(Accum acc, Part
                         unsigned qmid;
                         unsigned long long q = 0;
                         bool fxp;
-                        if (acc.xs) {
+                        if (XS) {
                             fxp = fx_quant_exact(fx[j], x, q);
                         } else {
                             fxp = fx_path(fx[j], x);
@@ -651,7 +651,7 @@ __global__ void __launch_bounds__(PART_THREADS, 1) k_part_reduce(Accum acc, Part
                             const unsigned old = atomicAdd(&p_dsm[w0], qlo);
                             qmid += (old + qlo < old) ? 1u : 0u;
                         } else {  // outside the fixed range: f64 L2 reduction, offset only here
-                            if (acc.xs) xsum_add_double(acc.xs, B, ss[j], base + l, x, s_xr);
+                            if (XS) xsum_add_double(acc.xs, B, ss[j], base + l, x, s_xr);
                             else atomicAdd(&acc.sum[(uint64_t)ss[j] * B + base + l], x);
                             qmid = FX_OFFSET_MID;
                         }
@@ -678,7 +678,7 @@ __global__ void __launch_bounds__(PART_THREADS, 1) k_part_reduce(Accum acc, Part
             for (int j = 0; j < A; ++j) {
                 if (ss[j] >= 0) {
                     const uint32_t w0 = o_fx + (uint32_t)ss[j] * 3u * W + l;
-                    if (acc.xs) {
+                    if (XS) {
                         xsum_add_fixed(acc.xs, B, ss[j], b, p_dsm[w0], p_dsm[w0 + W], p_dsm[w0 + 2 * W], cnt,
                                        FX_OFFSET, fx[j].F, s_xr);
                     } else {
@@ -697,7 +697,7 @@ __global__ void __launch_bounds__(PART_THREADS, 1) k_part_reduce(Accum acc, Part
         }
         __syncthreads();
     }
-    if (acc.xs) xr_publish(s_xr, acc.nsum, acc.xrange);  // (after the last tile's barrier)
+    if (XS) xr_publish(s_xr, acc.nsum, acc.xrange);  // (after the last tile's barrier)
 }
 
 // ---------------------------------------------------------------- host side
@@ -805,7 +805,7 @@ static cudaError_t launch_part_tail(const Inputs &in, const Accum &acc, const Pa
         *launches = 6;
     }
     const size_t sm3 = reduce_smem(acc, pa);
-    auto k3 = k_part_reduce<A>;
+    auto k3 = acc.xs ? k_part_reduce<A, true> : k_part_reduce<A, false>;
     if ((e = cudaFuncSetAttribute(k3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm3)) != cudaSuccess) return e;
     k3<<<pa.C / 2, PART_THREADS, sm3, s>>>(acc, pa);  // one 1024-thread CTA per SM (C = 2 x SMs)
     return cudaGetLastError();

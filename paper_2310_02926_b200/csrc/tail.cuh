@@ -54,17 +54,38 @@ __device__ __forceinline__ void finalize_body(const Geom &g, const Accum &acc, M
             }
         }
     } else if (G.ok) {
+        // several attributes: a chunk's loads are all issued before its stores
+        // (the stores may alias the loaded arrays as far as the compiler knows,
+        // so a load-divide-store loop waited for every load in turn)
+        constexpr int FC = 8;
         for (int64_t b = t0; b < (int64_t)nb; b += stride) {
             const unsigned long long cnt = __ldcg(acc.count + b);
             const double dc = (double)cnt;
-            for (int s = 0; s < acc.nsum; ++s) {
-                const double sm = __ldcg(acc.sum + (uint64_t)s * nb + b);
-                acc.oavg[(uint64_t)s * nb + b] = cnt ? __ddiv_rn(sm, dc) : __longlong_as_double(0x7ff8000000000000ll);
+            for (int s0 = 0; s0 < acc.nsum; s0 += FC) {
+                double sv[FC];
+#pragma unroll
+                for (int u = 0; u < FC; ++u)
+                    sv[u] = s0 + u < acc.nsum ? __ldcg(acc.sum + (uint64_t)(s0 + u) * nb + b) : 0.0;
+#pragma unroll
+                for (int u = 0; u < FC; ++u)
+                    if (s0 + u < acc.nsum)
+                        acc.oavg[(uint64_t)(s0 + u) * nb + b] =
+                            cnt ? __ddiv_rn(sv[u], dc) : __longlong_as_double(0x7ff8000000000000ll);
             }
-            for (int s = 0; s < acc.nmm; ++s) {
-                const ulonglong2 m = __ldcg((const ulonglong2 *)acc.mm + (uint64_t)s * nb + b);
-                acc.omin[(uint64_t)s * nb + b] = cnt ? dec_total(m.x) : __longlong_as_double(0x7ff0000000000000ll);
-                acc.omax[(uint64_t)s * nb + b] = cnt ? dec_total(~m.y) : __longlong_as_double((long long)0xfff0000000000000ull);
+            for (int s0 = 0; s0 < acc.nmm; s0 += FC) {
+                ulonglong2 mv[FC];
+#pragma unroll
+                for (int u = 0; u < FC; ++u)
+                    mv[u] = s0 + u < acc.nmm ? __ldcg((const ulonglong2 *)acc.mm + (uint64_t)(s0 + u) * nb + b)
+                                             : make_ulonglong2(0ull, 0ull);
+#pragma unroll
+                for (int u = 0; u < FC; ++u)
+                    if (s0 + u < acc.nmm) {
+                        acc.omin[(uint64_t)(s0 + u) * nb + b] =
+                            cnt ? dec_total(mv[u].x) : __longlong_as_double(0x7ff0000000000000ll);
+                        acc.omax[(uint64_t)(s0 + u) * nb + b] =
+                            cnt ? dec_total(~mv[u].y) : __longlong_as_double((long long)0xfff0000000000000ull);
+                    }
             }
         }
     }
