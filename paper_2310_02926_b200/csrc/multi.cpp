@@ -36,7 +36,7 @@ struct MSlot {
     Meta *meta_d = nullptr;            // [K]
     Meta *meta_h = nullptr;            // pinned mirror
     bool meta_valid = false;
-    cudaEvent_t done = nullptr, released = nullptr;
+    cudaEvent_t done = nullptr, released = nullptr, zeroed = nullptr;
     cudaEvent_t ev[MEV_N] = {};
     bool recd[MEV_N] = {};
     bool prof_pending = false;
@@ -56,6 +56,7 @@ struct bin_multi {
     int rank = 0, nranks = 1, device = 0;
     ncclComm_t comm = nullptr;
     cudaStream_t side = nullptr, copy = nullptr, meta_stream = nullptr;
+    cudaStream_t prep = nullptr;  // accumulator identities of the next slot, off the critical path
     MSlot slot[2];
     uint64_t next_ticket = 1;
     void *stage[2][BIN_MULTI_MAX_COLS] = {};
@@ -187,6 +188,7 @@ static int alloc_mslot(bin_multi *m, MSlot &S) {
     memset(S.meta_h, 0, (size_t)K * sizeof(Meta));
     DB_CUDA(cudaEventCreateWithFlags(&S.done, cudaEventDisableTiming));
     DB_CUDA(cudaEventCreateWithFlags(&S.released, cudaEventDisableTiming));
+    DB_CUDA(cudaEventCreateWithFlags(&S.zeroed, cudaEventDisableTiming));
     for (auto &ev : S.ev) DB_CUDA(cudaEventCreate(&ev));
     return BIN_OK;
 }
@@ -204,7 +206,8 @@ static void free_mslot(bin_multi *m, MSlot &S) {
     S.meta_h = nullptr;
     if (S.done) cudaEventDestroy(S.done);
     if (S.released) cudaEventDestroy(S.released);
-    S.done = S.released = nullptr;
+    if (S.zeroed) cudaEventDestroy(S.zeroed);
+    S.done = S.released = S.zeroed = nullptr;
     for (auto &e : S.ev)
         if (e) cudaEventDestroy(e), e = nullptr;
 }
@@ -320,6 +323,8 @@ int bin_multi_init(const bin_multi_op_t *ops, int32_t nops, int32_t ncols, const
         return fail(cuda_error(ce, "cudaStreamCreate"));
     if ((ce = cudaStreamCreateWithFlags(&m->copy, cudaStreamNonBlocking)) != cudaSuccess)
         return fail(cuda_error(ce, "cudaStreamCreate"));
+    if ((ce = cudaStreamCreateWithFlags(&m->prep, cudaStreamNonBlocking)) != cudaSuccess)
+        return fail(cuda_error(ce, "cudaStreamCreate"));
     if ((ce = cudaStreamCreateWithFlags(&m->meta_stream, cudaStreamNonBlocking)) != cudaSuccess)
         return fail(cuda_error(ce, "cudaStreamCreate"));
     for (int d = 0; d < n_a; ++d) {  // NVLink peer copies of columns that live on another GPU
@@ -385,6 +390,22 @@ int bin_multi_execute(bin_multi_t *m, bin_array_t *const *cols, int32_t ncols, u
     S.launches = 0;
     m->last = s;
     for (bool &r : S.recd) r = false;
+    // ---- a3 for all K on the prep stream, as soon as the slot's previous
+    // execute is done (typically while the other slot's execute still runs)
+    if (S.xs && n >= (1ll << 30))
+        return set_error(BIN_EINVAL, "BIN_SUM_EXACT: %lld rows per execute (limit 2^30)", (long long)n);
+    {
+        MultiArgs ai{};
+        ai.nops = m->K;
+        ai.ops = S.ops_d;
+        if (had) DB_CUDA(cudaStreamWaitEvent(m->prep, S.done, 0));
+        cudaError_t e0 = launch_multi_init(ai, m->max_work, m->prep);
+        if (e0 != cudaSuccess) return cuda_error(e0, "multi init kernel");
+        S.launches++;
+        if (S.xs)  // exact sums: digits cleared; reset every instance's touched range
+            DB_CUDA(cudaMemsetAsync(S.xrange, 0x7f, (size_t)m->K * 2 * BIN_MAX_ATTR * 4, m->prep));
+        DB_CUDA(cudaEventRecord(S.zeroed, m->prep));
+    }
     // ---- a1: view resolution (zero copy on the analysis device, else staged)
     MultiArgs a{};
     a.n = n;
@@ -465,14 +486,7 @@ int bin_multi_execute(bin_multi_t *m, bin_array_t *const *cols, int32_t ncols, u
     int rc;
     if ((rc = rec(MEV_START, true))) return rc;
     cudaError_t e;
-    // ---- a3 for all K
-    if ((e = launch_multi_init(a, m->max_work, s)) != cudaSuccess) return cuda_error(e, "multi init kernel");
-    S.launches++;
-    if (S.xs) {  // exact sums: digits cleared; reset every instance's touched range
-        if (n >= (1ll << 30))
-            return set_error(BIN_EINVAL, "BIN_SUM_EXACT: %lld rows per execute (limit 2^30)", (long long)n);
-        DB_CUDA(cudaMemsetAsync(S.xrange, 0x7f, (size_t)m->K * 2 * BIN_MAX_ATTR * 4, s));
-    }
+    DB_CUDA(cudaStreamWaitEvent(s, S.zeroed, 0));  // identities (enqueued on the prep stream above)
     if ((rc = rec(MEV_INIT, true))) return rc;
     // ---- a2 for every auto-bounded axis column (+ cross-rank Min)
     if (m->bound_cols) {
@@ -674,7 +688,11 @@ int bin_multi_finalize(bin_multi_t *m) {
         if (m->side) cudaStreamDestroy(m->side);
         if (m->copy) cudaStreamDestroy(m->copy);
         if (m->meta_stream) cudaStreamDestroy(m->meta_stream);
-        m->side = m->copy = m->meta_stream = nullptr;
+        if (m->prep) {
+            cudaStreamSynchronize(m->prep);
+            cudaStreamDestroy(m->prep);
+        }
+        m->side = m->copy = m->meta_stream = m->prep = nullptr;
     }
     m->finalized = true;
     delete m;
