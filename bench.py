@@ -50,6 +50,7 @@ def parse():
     p.add_argument("--bounds-auto", action="store_true")
     p.add_argument("--deterministic", action="store_true")
     p.add_argument("--exact", action="store_true", help="BIN_SUM_EXACT: correctly rounded exact sums (R20)")
+    p.add_argument("--rows", type=int, default=0, help="experiments only: override the workload's total rows")
     return p.parse_args()
 
 
@@ -216,7 +217,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     w = synth.CONFIGS[args.workload]
-    N_total = w.n * (world if args.scaling == "weak" else 1)
+    N_total = (args.rows or w.n) * (world if args.scaling == "weak" else 1)
     r0, r1 = shard(N_total, rank, world)
     n = r1 - r0
     stream = torch.cuda.Stream(dev)

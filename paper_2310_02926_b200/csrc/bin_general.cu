@@ -32,7 +32,15 @@ namespace db {
 
 extern __shared__ __align__(16) uint32_t g_dsm[];
 
+// This file is compiled twice: as itself (BIN_SUM_FAST instances + the
+// dispatching launcher) and through bin_general_x.cu with BIN_GENERAL_XS = 1
+// (the BIN_SUM_EXACT instances), so the two sets build in parallel.
+#ifndef BIN_GENERAL_XS
+#define BIN_GENERAL_XS 0
+#endif
+#if !BIN_GENERAL_XS
 int window_bytes_per_bin(const Accum &acc) { return 4 + 12 * acc.nsum + 8 * acc.nmm; }
+#endif
 
 struct GenCtx {
     DGeom G;
@@ -293,8 +301,8 @@ static cudaError_t launch_general(const Geom &g, const Inputs &in, const Accum &
     int blocks = lc.sms;  // one persistent CTA per SM: the whole shared memory holds the window
     const int64_t maxb = (in.n + T - 1) / T;
     if (maxb < blocks) blocks = (int)(maxb > 0 ? maxb : 1);
-    auto kern = acc.xs ? (vec ? k_bin<D, A, true, true> : k_bin<D, A, false, true>)
-                       : (vec ? k_bin<D, A, true, false> : k_bin<D, A, false, false>);
+    constexpr bool XS = BIN_GENERAL_XS != 0;
+    auto kern = vec ? k_bin<D, A, true, XS> : k_bin<D, A, false, XS>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     kern<<<blocks, T, smem, s>>>(g, in, acc, vec ? head : 0);
@@ -311,8 +319,16 @@ static cudaError_t launch_general_d(const Geom &g, const Inputs &in, const Accum
     return launch_general<D, 16>(g, in, acc, lc, smem, s);
 }
 
+#if BIN_GENERAL_XS
+cudaError_t launch_bin_general_exact(const Geom &g, const Inputs &in, const Accum &acc, const LaunchCfg &lc, int smem,
+                                     cudaStream_t s) {
+#else
+cudaError_t launch_bin_general_exact(const Geom &g, const Inputs &in, const Accum &acc, const LaunchCfg &lc, int smem,
+                                     cudaStream_t s);
 cudaError_t launch_bin_general(const Geom &g, const Inputs &in, const Accum &acc, const LaunchCfg &lc, int smem,
                                cudaStream_t s) {
+    if (acc.xs) return launch_bin_general_exact(g, in, acc, lc, smem, s);
+#endif
     switch (g.ndim) {
     case 1: return launch_general_d<1>(g, in, acc, lc, smem, s);
     case 2: return launch_general_d<2>(g, in, acc, lc, smem, s);
