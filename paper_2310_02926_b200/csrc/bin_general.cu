@@ -316,6 +316,7 @@ static cudaError_t launch_general_d(const Geom &g, const Inputs &in, const Accum
     if (na == 0) return launch_general<D, 0>(g, in, acc, lc, smem, s);
     if (na == 1) return launch_general<D, 1>(g, in, acc, lc, smem, s);
     if (na <= 4) return launch_general<D, 4>(g, in, acc, lc, smem, s);
+    if (na <= 8) return launch_general<D, 8>(g, in, acc, lc, smem, s);  // (the A = 16 instance spills)
     return launch_general<D, 16>(g, in, acc, lc, smem, s);
 }
 
