@@ -167,8 +167,10 @@ typedef struct {
                                    BIN_SUM_EXACT: every bin's sum is its exact real sum rounded once
                                    to nearest-even (R20; zero -> +0.0, beyond DBL_MAX ->
                                    +-inf), avg = that sum / count -- identical across runs, routes and
-                                   rank counts.  Needs finite attribute values (R7), fewer than 2^30
-                                   rows per execute and rank, and deterministic == 0 (else BIN_EINVAL);
+                                   rank counts.  Needs finite attribute values (R7), fewer than
+                                   2^30 / nranks rows per execute and rank (all ranks' rows < 2^30:
+                                   digit headroom of the cross-rank add), and deterministic == 0
+                                   (else BIN_EINVAL);
                                    costs 66 x 8 bytes per bin and summed attribute of device memory. */
 } bin_spec_t;
 enum { BIN_ROUTE_AUTO = 0, BIN_ROUTE_WINDOW = 1, BIN_ROUTE_PARTITION = 2 };
@@ -235,9 +237,10 @@ typedef struct {
 void bin_placement_default(bin_placement_t *p);
 
 /* Eq. (1): d = ((r mod n_u) * s + d_0) mod n_a  (reading R14),
- * or the explicit device.  Host-only, needs no GPU.  n_avail = n_a.
- * Errors: BIN_ENOTSUP (device_id == -1), BIN_EDEVICE (explicit id out of
- * range, n_avail < 1), BIN_EINVAL (stride < 1, device_start < 0). */
+ * or the explicit device, wrapped modulo n_a like Eq. (1) itself (reading
+ * R14b).  Host-only, needs no GPU.  n_avail = n_a.
+ * Errors: BIN_ENOTSUP (device_id == -1), BIN_EDEVICE (device_id < -2 or
+ * n_avail < 1), BIN_EINVAL (stride < 1, device_start < 0). */
 int bin_resolve_device(const bin_placement_t *p, int32_t rank, int32_t n_avail,
                        int32_t *device);
 

@@ -61,6 +61,14 @@ def _load():
     return _lib
 
 
+class Degenerate(ValueError):
+    """Auto bounds with no usable mesh (the library's BIN_EDEGENERATE)."""
+
+
+class InvalidArgument(ValueError):
+    """Bad arguments, e.g. unusable manual bounds (the library's BIN_EINVAL)."""
+
+
 def _dptr(a: np.ndarray):
     return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
 
@@ -114,8 +122,12 @@ def databin(axes, attrs, res, lo=None, hi=None, bounds_auto=False, P=1, exact=Fa
         _dptr(loa), _dptr(hia), int(P), n, _ptr_array(axes), nattr, _ptr_array(attrs),
         count.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), _dptr(s), _dptr(sa),
         _dptr(mn), _dptr(mx), _dptr(avg), ctypes.byref(n_in), ctypes.byref(n_out))
+    if rc == -1:
+        raise Degenerate("auto bounds: no non-NaN row on an axis, or realised bounds not usable (reading R4)")
+    if rc == -3:
+        raise InvalidArgument("bad arguments or unusable manual bounds (reading R4)")
     if rc != 0:
-        raise ValueError(f"oracle_databin failed rc={rc}")
+        raise MemoryError(f"oracle_databin failed rc={rc}")
     k = slice(0, nattr)
     out = dict(count=count, sum=s[k], sumabs=sa[k], min=mn[k], max=mx[k], avg=avg[k],
                n_in=int(n_in.value), n_out=int(n_out.value),

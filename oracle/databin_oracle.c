@@ -94,6 +94,21 @@ int oracle_expand_degenerate(int ndim, double *lo, double *hi)
     return 0;
 }
 
+/* Reading R4: the mesh of an axis is usable only if lo < hi, both are finite,
+ * and the width hi - lo and the scale res / (hi - lo) are finite (else the
+ * index (x - lo) * scale of some in-bounds x is NaN or infinite and has no
+ * bin).  Auto bounds that fail this are degenerate (-1 from oracle_databin);
+ * manual ones are invalid arguments (-3).  Returns 1 when usable. */
+int oracle_bounds_usable(int ndim, const int32_t *res, const double *lo, const double *hi)
+{
+    for (int d = 0; d < ndim; ++d) {
+        if (!(lo[d] < hi[d]) || isinf(lo[d]) || isinf(hi[d])) return 0;
+        double w = hi[d] - lo[d];
+        if (isinf(w) || isinf((double)res[d] / w)) return 0;
+    }
+    return 1;
+}
+
 /* ---- Empty grid: the identity of every reduction (reading R5) ---- */
 void oracle_grid_init(int64_t nbins, int nattr, uint64_t *count, double *sum,
                       double *sumabs, double *vmin, double *vmax)
@@ -198,8 +213,9 @@ void oracle_finalize(int64_t nbins, int nattr, const uint64_t *count,
  * grid, and the grids are folded in rank order 0..P-1 onto the empty grid.
  * P = 1 is the plain sequential loop.
  * bounds_auto: lo/hi are outputs (global min/max, then reading R4).
- * Returns 0, -1 (auto bounds on N == 0 or unrecoverable degenerate axis),
- * -2 (allocation failure), -3 (bad arguments). */
+ * Returns 0, -1 (auto bounds on N == 0, an axis with no non-NaN value, or
+ * realised bounds that are not usable -- reading R4), -2 (allocation
+ * failure), -3 (bad arguments, unusable manual bounds included). */
 int oracle_databin(int ndim, const int32_t *res, int bounds_auto,
                    double *lo, double *hi, int P, int64_t n,
                    const double *const *axes, int nattr,
@@ -218,9 +234,9 @@ int oracle_databin(int ndim, const int32_t *res, int bounds_auto,
     if (bounds_auto) {
         if (oracle_bounds(ndim, n, axes, lo, hi) != 0) return -1;
         if (oracle_expand_degenerate(ndim, lo, hi) != 0) return -1;
+        if (!oracle_bounds_usable(ndim, res, lo, hi)) return -1;
     }
-    for (int d = 0; d < ndim; ++d)
-        if (!(lo[d] < hi[d])) return -3;
+    if (!oracle_bounds_usable(ndim, res, lo, hi)) return -3;
 
     *n_in = 0;
     *n_out = 0;

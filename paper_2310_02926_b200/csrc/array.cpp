@@ -109,18 +109,31 @@ int array_mark_use(bin_array *a, cudaStream_t s, int dev) {
     for (bin_array *x = a; x; x = x->source) {
         std::lock_guard<std::mutex> lk(x->mu);
         DeviceGuard g(dev);
-        if (x->last_use && x->last_use_device != dev) {
-            DeviceGuard g2(x->last_use_device);
-            cudaEventDestroy(x->last_use);
-            x->last_use = nullptr;
+        bin_array::Use *u = nullptr;
+        for (auto &r : x->uses)
+            if (r.device == dev && r.stream == s) u = &r;
+        if (!u) {
+            cudaEvent_t ev;
+            DB_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+            x->uses.push_back({dev, s, ev});
+            u = &x->uses.back();
         }
-        if (!x->last_use) {
-            DB_CUDA(cudaEventCreateWithFlags(&x->last_use, cudaEventDisableTiming));
-            x->last_use_device = dev;
-        }
-        DB_CUDA(cudaEventRecord(x->last_use, s));
+        DB_CUDA(cudaEventRecord(u->ev, s));  // supersedes only this stream's earlier use
     }
     return BIN_OK;
+}
+
+// waits for every recorded use; destroy: also drop the events
+static cudaError_t drain_uses(bin_array *x, bool destroy) {
+    cudaError_t rc = cudaSuccess;
+    for (auto &u : x->uses) {
+        DeviceGuard g(u.device);
+        cudaError_t e = cudaEventSynchronize(u.ev);
+        if (e != cudaSuccess && rc == cudaSuccess) rc = e;
+        if (destroy) cudaEventDestroy(u.ev);
+    }
+    if (destroy) x->uses.clear();
+    return rc;
 }
 
 static size_t elem_size(int32_t dtype) { return dtype == BIN_F64 ? 8 : 0; }
@@ -339,10 +352,8 @@ int bin_array_synchronize(bin_array_t *a) {
     if (!a) return set_error(BIN_EINVAL, "bin_array_synchronize: NULL array");
     for (bin_array *x = a; x; x = x->source) {
         std::lock_guard<std::mutex> lk(x->mu);
-        if (x->last_use) {
-            cudaError_t e = cudaEventSynchronize(x->last_use);
-            if (e != cudaSuccess) return cuda_error(e, "bin_array_synchronize");
-        }
+        cudaError_t e0 = drain_uses(x, false);
+        if (e0 != cudaSuccess) return cuda_error(e0, "bin_array_synchronize");
         if (x->stream && (x->device >= 0 || x->alloc == BIN_ALLOC_HOST_PINNED)) {
             DeviceGuard g(x->device);
             cudaError_t e = cudaStreamSynchronize(x->stream);
@@ -355,12 +366,7 @@ int bin_array_synchronize(bin_array_t *a) {
 void bin_array_release(bin_array_t *a) {
     while (a) {
         if (--a->refs > 0) return;
-        if (a->last_use) {  // drain library work that reads/writes this memory
-            DeviceGuard g(a->last_use_device);
-            cudaEventSynchronize(a->last_use);
-            cudaEventDestroy(a->last_use);
-            a->last_use = nullptr;
-        }
+        drain_uses(a, true);  // library work on any stream/GPU that reads/writes this memory
         free_storage(a);
         bin_array *src = a->source;
         delete a;

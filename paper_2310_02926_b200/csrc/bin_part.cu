@@ -7,11 +7,13 @@
 //   P1 k_part_keys     read the axes, write each row's bin index (u32, ~0 when
 //                      outside), count rows per tile (shared memory, then one
 //                      L2 add per tile and CTA)
-//   P2 k_part_scan     one CTA: tile starts (exclusive scan) and cursors
+//   P2 k_part_scan1/2  per-tile prefix over chunks, tile starts and the
+//                      per-(group, chunk) write offsets: every output position
+//                      is known before the scatter (no L2 atomic claims)
 //   P3 k_part_scatter  read keys + attributes (cp.async double buffer),
 //                      counting-sort each batch of rows by group in shared
-//                      memory, claim each group's range with one L2 atomic,
-//                      write the rows out as contiguous runs (coalesced).
+//                      memory, write the rows out as contiguous runs at the
+//                      offsets of P2 (coalesced).
 //                      Group = tile when T <= 64; else a super-tile of G1
 //                      consecutive tiles (<= 64 of them), and
 //   P3' k_part_refine  regroups each super-tile's rows by tile the same way, so

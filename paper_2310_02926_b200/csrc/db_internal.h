@@ -6,6 +6,7 @@
 #include <atomic>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/databin.h"
 
@@ -61,8 +62,15 @@ struct bin_array {
     void (*release)(void *, void *) = nullptr;
     void *release_ctx = nullptr;
     bin_array *source = nullptr;  // views keep their source alive
-    cudaEvent_t last_use = nullptr;  // last library work reading/writing this memory
-    int last_use_device = -1;
+    // library work reading/writing this memory: the last event recorded on each
+    // (device, stream) that used it -- release/synchronize wait for all of them
+    // (one event per array would cover only the most recent user)
+    struct Use {
+        int device;
+        cudaStream_t stream;
+        cudaEvent_t ev;
+    };
+    std::vector<Use> uses;
     std::mutex mu;
 };
 
@@ -183,6 +191,7 @@ struct PeerSet {
     int32_t *xrange[PEER_MAX];
     unsigned long long *flags[PEER_MAX];  // every rank's barrier words [A: 0..63][B: 64..127]
     unsigned *ctas_done;                  // this rank's last-CTA counter
+    unsigned *ctas_failed;                // nonzero: a CTA of this rank timed out at barrier A
 };
 cudaError_t launch_combine_peer(const Geom &g, const PeerSet &ps, int rank, int nranks, unsigned long long epoch,
                                 Meta *meta, int variant, int deterministic, int sms, cudaStream_t s);

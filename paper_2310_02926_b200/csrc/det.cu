@@ -27,59 +27,14 @@
 #include <stdint.h>
 
 #include "db_internal.h"
+#include "dev_common.cuh"
 
 namespace db {
-
-__device__ __forceinline__ unsigned long long enc_total_d(double x) {
-    unsigned long long b = (unsigned long long)__double_as_longlong(x);
-    unsigned long long m = (unsigned long long)((long long)b >> 63);
-    return b ^ (m | 0x8000000000000000ull);
-}
-
-// ---- geometry (same definition as kernels.cu, restated) ----
-struct DetGeom {
-    double lo[3], scale[3], hi[3];
-    int res[3];
-    bool ok;
-};
-
-__device__ __forceinline__ double dec_total_d(unsigned long long e) {
-    unsigned long long m = ~(unsigned long long)((long long)e >> 63);
-    return __longlong_as_double((long long)(e ^ (m | 0x8000000000000000ull)));
-}
-
-__device__ DetGeom det_geom(const Geom &g, const unsigned long long *bounds) {
-    DetGeom G;
-    G.ok = true;
-    for (int d = 0; d < 3; ++d) {
-        G.res[d] = d < g.ndim ? g.res[d] : 1;
-        G.lo[d] = 0.0;
-        G.hi[d] = 1.0;
-        G.scale[d] = 1.0;
-        if (d >= g.ndim) continue;
-        double lo = g.lo[d], hi = g.hi[d];
-        if (g.bounds_auto) {
-            unsigned long long elo = bounds[d], nhi = bounds[g.ndim + d];
-            if (elo == ~0ull || nhi == ~0ull) G.ok = false;
-            lo = dec_total_d(elo);
-            hi = dec_total_d(~nhi);
-            if (lo == hi) {
-                lo = __dsub_rn(lo, 0.5);
-                hi = __dadd_rn(hi, 0.5);
-            }
-            if (!(lo < hi) || isinf(lo) || isinf(hi)) G.ok = false;
-        }
-        G.lo[d] = lo;
-        G.hi[d] = hi;
-        G.scale[d] = __ddiv_rn((double)G.res[d], __dsub_rn(hi, lo));
-    }
-    return G;
-}
 
 // payload: VALS ? the value of attribute `va` : the row index (as u32 in the low word)
 template <bool VALS>
 __global__ void __launch_bounds__(256) k_det_keys(Geom g, Inputs in, Accum acc, uint32_t *keys, void *payload, int va) {
-    DetGeom G = det_geom(g, acc.bounds);
+    const DGeom G = load_geom(g, acc.bounds);
     const uint32_t B = (uint32_t)acc.nbins;
     uint32_t n_in = 0, n_seen = 0;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -103,7 +58,7 @@ __global__ void __launch_bounds__(256) k_det_keys(Geom g, Inputs in, Accum acc, 
             for (int d = 0; d < 3; ++d) {
                 if (d >= g.ndim) break;
                 inside = inside && (G.lo[d] <= x[u][d]) && (x[u][d] <= G.hi[d]);
-                int kd = min(__double2loint(__dadd_rd(__dmul_rn(__dsub_rn(x[u][d], G.lo[d]), G.scale[d]), 4503599627370496.0)), G.res[d] - 1);  // floor (see dev_common.cuh floor_nonneg)
+                int kd = min(floor_nonneg(__dmul_rn(__dsub_rn(x[u][d], G.lo[d]), G.scale[d])), G.res[d] - 1);
                 b += (uint32_t)kd * mul;
                 mul *= (uint32_t)G.res[d];
             }
@@ -397,7 +352,7 @@ __global__ void __launch_bounds__(256) k_det_fold(Inputs in, Accum acc, const vo
                     if (j + k >= j1) break;
                     if (want_sum) s = __dadd_rn(s, v[k]);
                     if (want_mm) {
-                        const unsigned long long e = enc_total_d(v[k]);
+                        const unsigned long long e = enc_total(v[k]);
                         emin = e < emin ? e : emin;
                         nemax = ~e < nemax ? ~e : nemax;
                     }
@@ -445,7 +400,7 @@ __global__ void __launch_bounds__(256) k_det_fold_long(Inputs in, Accum acc, con
                 for (int u = 0; u < PER; ++u) {
                     const uint32_t j = j0 + c * CH + u * 32 + lane;
                     if (want_mm && j < j1) {
-                        const unsigned long long e = enc_total_d(r[u]);
+                        const unsigned long long e = enc_total(r[u]);
                         emin = e < emin ? e : emin;
                         nemax = ~e < nemax ? ~e : nemax;
                     }

@@ -66,11 +66,14 @@ __device__ __forceinline__ DGeom load_geom(const Geom &g, const unsigned long lo
                 lo = __dsub_rn(lo, 0.5);
                 hi = __dadd_rn(hi, 0.5);
             }
-            if (!(lo < hi) || isinf(lo) || isinf(hi)) G.ok = false;
         }
         G.lo[d] = lo;
         G.hi[d] = hi;
         G.scale[d] = __ddiv_rn((double)G.res[d], __dsub_rn(hi, lo));
+        // reading R4: usable bounds are finite, lo < hi, with a finite width and
+        // scale (manual bounds are checked the same way at bin_init)
+        if (g.bounds_auto && (!(lo < hi) || isinf(lo) || isinf(hi) || isinf(__dsub_rn(hi, lo)) || isinf(G.scale[d])))
+            G.ok = false;
     }
     return G;
 }

@@ -279,8 +279,7 @@ int bin_resolve_device(const bin_placement_t *p, int32_t rank, int32_t n_avail, 
     if (p->device_id == BIN_DEVICE_HOST)
         return set_error(BIN_ENOTSUP, "host placement (device_id = -1): this library has no CPU path");
     if (p->device_id >= 0) {
-        if (p->device_id >= n_avail) return set_error(BIN_EDEVICE, "device_id %d >= %d devices", p->device_id, n_avail);
-        *device = p->device_id;
+        *device = p->device_id % n_avail;  // explicit ids wrap like Eq. (1) (reading R14b)
         return BIN_OK;
     }
     if (p->device_id != BIN_DEVICE_AUTO) return set_error(BIN_EDEVICE, "device_id %d", p->device_id);
@@ -388,6 +387,7 @@ static bool setup_peer(bin_handle *h) {
         PeerSet &ps = S.peers;
         ps.me = S.acc;
         ps.ctas_done = h->ctas_done + k;
+        ps.ctas_failed = h->ctas_done + 4 + k;
         auto rel = [&](const void *local, int p) {
             return slot_base[p][k] + ((const unsigned char *)local - S.base);
         };
@@ -732,8 +732,12 @@ static int execute_impl(bin_handle *h, bin_array_t *const *axes, int32_t naxes, 
     };
     int rc;
     if ((rc = rec(EV_INIT0, staged_any))) return rc;
-    if (S.acc.xs && n >= (1ll << 30))
-        return set_error(BIN_EINVAL, "BIN_SUM_EXACT: %lld rows per execute (limit 2^30: digit headroom)", (long long)n);
+    // exact sums: every digit stays below 2^62 in magnitude only while the rows of
+    // ALL ranks together stay below 2^30 (the cross-rank combine adds the ranks'
+    // digits before it normalises the carries), so each rank takes < 2^30 / nranks
+    if (S.acc.xs && n >= (1ll << 30) / h->nranks)
+        return set_error(BIN_EINVAL, "BIN_SUM_EXACT: %lld rows per execute and rank (limit 2^30 / %d ranks: digit headroom)",
+                         (long long)n, h->nranks);
     // ---- route: partition (bin_part.cu) or window; auto follows the last probe
     PartArgs pa{};
     const bool part_ok = n > 0 && !h->spec.deterministic && h->spec.route != BIN_ROUTE_WINDOW &&

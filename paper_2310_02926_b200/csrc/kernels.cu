@@ -7,7 +7,9 @@
 //   k_bin       bin index (a4) + accumulate (a5): CTA-private window in
 //               shared memory, global L2 reductions for the rest
 //   k_finalize  avg = sum/count, decode min/max, sentinels        [a7]
-// The cross-rank combine (a6) is NCCL, enqueued by handle.cpp.
+// The cross-rank combine (a6) is the fused NVLink peer kernel of
+// combine_peer.cu by default (NCCL allreduce + k_finalize as the fallback,
+// DATABIN_COMBINE=nccl), enqueued by handle.cpp.
 //
 // Arithmetic contract shared with the oracle by *definition* (not code):
 //   scale_d = (double)res_d / (hi_d - lo_d)        (IEEE div, once per CTA)

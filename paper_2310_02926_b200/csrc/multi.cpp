@@ -392,8 +392,9 @@ int bin_multi_execute(bin_multi_t *m, bin_array_t *const *cols, int32_t ncols, u
     for (bool &r : S.recd) r = false;
     // ---- a3 for all K on the prep stream, as soon as the slot's previous
     // execute is done (typically while the other slot's execute still runs)
-    if (S.xs && n >= (1ll << 30))
-        return set_error(BIN_EINVAL, "BIN_SUM_EXACT: %lld rows per execute (limit 2^30)", (long long)n);
+    if (S.xs && n >= (1ll << 30) / m->nranks)  // all ranks' rows < 2^30: digit headroom of the cross-rank add
+        return set_error(BIN_EINVAL, "BIN_SUM_EXACT: %lld rows per execute and rank (limit 2^30 / %d ranks)",
+                         (long long)n, m->nranks);
     {
         MultiArgs ai{};
         ai.nops = m->K;

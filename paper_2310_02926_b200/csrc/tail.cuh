@@ -122,14 +122,23 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
     return v;
 }
 
-// thread 0 of the calling CTA: wait until flags[p*stride] >= epoch for all p
-__device__ __forceinline__ bool wait_all(const unsigned long long *flags, int nranks, unsigned long long epoch) {
+// Barrier words hold the execute's epoch; barrier B's word also carries
+// PEER_FAIL when the publishing rank's combine did not complete (a CTA timed
+// out at barrier A and skipped its bins), so every rank reports BIN_ENCCL.
+constexpr unsigned long long PEER_FAIL = 1ull << 63;
+
+// thread 0 of the calling CTA: wait until (flags[p] & ~PEER_FAIL) >= epoch for
+// all p; false on timeout, *failed |= a peer published PEER_FAIL for `epoch`
+__device__ __forceinline__ bool wait_all(const unsigned long long *flags, int nranks, unsigned long long epoch,
+                                         bool *failed = nullptr) {
     const long long t0 = clock64();
     for (int p = 0; p < nranks; ++p) {
-        while (ld_acquire_sys(flags + p) < epoch) {
+        unsigned long long v;
+        while (((v = ld_acquire_sys(flags + p)) & ~PEER_FAIL) < epoch) {
             if (clock64() - t0 > SPIN_LIMIT_CYCLES) return false;
             __nanosleep(64);
         }
+        if (failed && (v & PEER_FAIL) && (v & ~PEER_FAIL) == epoch) *failed = true;
     }
     return true;
 }
@@ -311,7 +320,22 @@ __device__ __forceinline__ void combine_peer_body(const Geom &g, const PeerSet &
             for (int p = 0; p < nranks; ++p) st_release_sys(ps.flags[p] + rank, epoch);  // flagsA[rank] on peer p
         }
         ok_s = wait_all(ps.flags[rank], nranks, epoch);
-        if (blockIdx.x == 0) meta->trace[1] = globaltimer();
+        if (!ok_s) atomicOr(ps.ctas_failed, 1u);  // this CTA skips its bins: the rank's combine failed
+        if (blockIdx.x == 0) {
+            meta->trace[1] = globaltimer();
+            if (ok_s) {
+                // n_in / n_out summed over the ranks now, while every rank's words are
+                // final: after barrier B a peer may already re-zero them for its next
+                // execute on this slot
+                unsigned long long nin = 0, nout = 0;
+                for (int p = 0; p < nranks; ++p) {
+                    nin += __ldcg(ps.count[p] + B);
+                    nout += __ldcg(ps.count[p] + B + 1);
+                }
+                meta->n_in = nin;
+                meta->n_out = nout;
+            }
+        }
     }
     __syncthreads();
     const bool ok = ok_s;
@@ -403,20 +427,15 @@ __device__ __forceinline__ void combine_peer_body(const Geom &g, const PeerSet &
     if (threadIdx.x == 0) {
         meta->trace[2] = globaltimer();
         *ps.ctas_done = 0u;  // reset for the next execute (stream-ordered)
+        const bool failed = atomicExch(ps.ctas_failed, 0u) != 0u;  // some CTA of this rank timed out
         __threadfence_system();
-        for (int p = 0; p < nranks; ++p) st_release_sys(ps.flags[p] + 64 + rank, epoch);  // flagsB
-        const bool ok2 = ok && wait_all(ps.flags[rank] + 64, nranks, epoch);
-        // n_in / n_out (summed over ranks) and the result meta
-        unsigned long long nin = 0, nout = 0;
-        for (int p = 0; p < nranks; ++p) {
-            nin += __ldcg(ps.count[p] + B);
-            nout += __ldcg(ps.count[p] + B + 1);
-        }
+        const unsigned long long fb = epoch | (failed ? PEER_FAIL : 0ull);
+        for (int p = 0; p < nranks; ++p) st_release_sys(ps.flags[p] + 64 + rank, fb);  // flagsB
+        bool peer_failed = false;
+        const bool ok2 = !failed && wait_all(ps.flags[rank] + 64, nranks, epoch, &peer_failed) && !peer_failed;
         const DGeom G = load_geom(g, me.bounds);
         meta->status = !ok2 ? BIN_ENCCL : (G.ok ? 0 : BIN_EDEGENERATE);
         meta->variant = variant;
-        meta->n_in = nin;
-        meta->n_out = nout;
         for (int d = 0; d < 3; ++d) {
             meta->lo[d] = G.lo[d];
             meta->hi[d] = G.hi[d];

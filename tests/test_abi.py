@@ -58,7 +58,10 @@ def test_eq1_defaults_and_overrides(db):
     assert [db.bin_resolve_device(p, r, 4) for r in range(8)] == [0, 1, 2, 3, 0, 1, 2, 3]
     p.device_id = 2
     assert db.bin_resolve_device(p, 7, 4) == 2
-    p.device_id = 5
+    p.device_id = 5                                       # explicit ids wrap modulo n_a (R14b)
+    assert [db.bin_resolve_device(p, r, 4) for r in range(3)] == [1, 1, 1]
+    assert db.bin_resolve_device(p, 0, 5) == 0 and db.bin_resolve_device(p, 0, 6) == 5
+    p.device_id = -3
     with pytest.raises(db.BinError) as e:
         db.bin_resolve_device(p, 0, 4)
     assert e.value.code == db.capi.BIN_EDEVICE

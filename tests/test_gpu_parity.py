@@ -221,3 +221,33 @@ def test_c3_full_100M_plummer_512x512(db):
     inside_mass = float(np.sum(out["sum"][0]))
     assert 0 < out["n_out"] < w.n // 100                    # ~0.1% outside the +-16 a box
     assert inside_mass < tot
+
+
+# ---------------------------------------------------------------- unusable bounds (reading R4)
+@pytest.mark.parametrize("route", ["window", "partition"])
+@pytest.mark.parametrize("deterministic", [False, True])
+def test_unusable_auto_bounds_are_degenerate(db, route, deterministic):
+    # the oracle's pins (test_oracle.py) and the library agree: no mesh, BIN_EDEGENERATE
+    big = np.finfo(np.float64).max
+    cases = [[[0.0, 1.0, np.inf]], [[-np.inf, 0.0, 1.0]], [[-big, big]], [[0.0, 5e-324]], [[1e300, 1e300]],
+             [[0.0, 1.0], [0.0, np.inf]]]
+    for axes in cases:
+        with pytest.raises(oracle.Degenerate):
+            oracle.databin(axes, [np.ones(len(axes[0]))], [4] * len(axes), bounds_auto=True)
+        with pytest.raises(db.BinError) as e:
+            run_gpu(db, axes, [np.ones(len(axes[0]))], [4] * len(axes), bounds_auto=True, route=route,
+                    deterministic=deterministic)
+        assert e.value.code == db.capi.BIN_EDEGENERATE, axes
+    # NaN rows alone do not spoil the bounds (R4): same result as the oracle
+    both(db, [[0.0, np.nan, 1.0, 0.25]], [[1.0, 2.0, 3.0, 4.0]], [2], bounds_auto=True, exact=True, route=route)
+
+
+def test_unusable_manual_bounds_are_invalid(db):
+    big = np.finfo(np.float64).max
+    for lo, hi in ((0.0, np.inf), (-np.inf, 0.0), (np.nan, 1.0), (1.0, 1.0), (2.0, 1.0), (-big, big), (0.0, 5e-324)):
+        with pytest.raises(oracle.InvalidArgument):
+            oracle.databin([[0.5]], [[1.0]], [4], [lo], [hi])
+        with pytest.raises(db.BinError) as e:
+            run_gpu(db, [[0.5]], [[1.0]], [4], [lo], [hi])
+        assert e.value.code == db.capi.BIN_EINVAL, (lo, hi)
+    both(db, [[-big / 2, big / 4, big / 2]], [[1.0, 2.0, 3.0]], [2], [-big / 2], [big / 2], exact=True)

@@ -4,5 +4,5 @@ timeout 600 python -m pytest tests/test_gpu_placement.py tests/test_gpu_placemen
 timeout 900 python tools/placement_study.py --n 50000000 --steps 100 > gpurun_out/placement.jsonl 2> gpurun_out/placement.err; echo rc=$?
 cat gpurun_out/placement.jsonl
 export CUDA_VISIBLE_DEVICES=0
-VARIANTS="gfoff" bash tools/ab.sh
-BENCH_ARGS="--workload c5" VARIANTS="gfoff" bash tools/ab.sh
+VARIANTS="gfoff" bash tools/gpurun/ab.sh
+BENCH_ARGS="--workload c5" VARIANTS="gfoff" bash tools/gpurun/ab.sh
