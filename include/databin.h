@@ -279,6 +279,31 @@ int bin_execute(bin_handle_t *h, bin_array_t *const *axes, int32_t naxes,
 int bin_execute_shards(bin_handle_t *h, bin_array_t *const *axes, int32_t naxes,
                        bin_array_t *const *attrs, int32_t nattr, int32_t nshards, uint64_t *ticket);
 
+/* One-device rank group (PAPER.md:479 with Eq. (1): when there are
+ * more ranks than devices, several ranks bin on one GPU).  bin_init_group
+ * creates nranks (1..16) handles out[0..nranks) on ONE device (resolved from
+ * `place` for rank 0), rank r = out[r]; each bins only its own rows into its
+ * own accumulators, exactly as one process per GPU does, and the group's
+ * combine is the fused peer combine + finalize kernel of the multi-GPU path
+ * (same device code: barrier words, rank-order sum fold, exact-digit add,
+ * min/max, finalize, all-gather of the results into every rank) launched once
+ * for all ranks.  Results of rank r equal a multi-process run with nranks
+ * ranks -- in deterministic / exact mode the oracle's partition mode P = nranks
+ * bit for bit.  Manual bounds only (auto bounds: BIN_ENOTSUP).  Each handle
+ * is finalized with bin_finalize; bin_execute on a member is BIN_ESTATE.
+ * Errors: as bin_init; BIN_EINVAL for nranks outside 1..16 or NULL pointers. */
+int bin_init_group(const bin_spec_t *spec, const bin_placement_t *place, int32_t nranks, bin_handle_t **out);
+
+/* Collective execute of a rank group: h[r] (rank r, all nranks members in
+ * order) bins rank r's columns axes[r*naxes + d], attrs[r*nattr + a] on its
+ * own work stream (placement as bin_execute), then one launch combines and
+ * finalizes all ranks after every rank has binned; each rank's result is then
+ * available through bin_wait / bin_result on its own handle with the shared
+ * *ticket.  Errors: as bin_execute; BIN_ESTATE when a handle is not rank r of
+ * the group, was finalized, or the ranks' tickets differ. */
+int bin_execute_group(bin_handle_t *const *h, int32_t nranks, bin_array_t *const *axes, int32_t naxes,
+                      bin_array_t *const *attrs, int32_t nattr, uint64_t *ticket);
+
 /* Event after which the producer may overwrite the inputs of `ticket`
  * (snapshot copy done, or binning done when reading in place). */
 int bin_inputs_released(bin_handle_t *h, uint64_t ticket, bin_event_t *ev);

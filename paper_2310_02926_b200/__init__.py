@@ -166,6 +166,27 @@ def bin_execute_shards(h, shards):
     return t.value
 
 
+def bin_init_group(spec, nranks, placement=None):
+    """nranks handles (ranks 0..nranks-1) of a one-device rank group."""
+    out = (ctypes.c_void_p * int(nranks))()
+    pl = ctypes.byref(placement) if placement is not None else None
+    check(_lib.bin_init_group(ctypes.byref(spec), pl, int(nranks), out), "bin_init_group")
+    return [x for x in out]
+
+
+def bin_execute_group(hs, shards):
+    """shards[r] = (axes, attrs) array handles of rank r; returns the shared ticket."""
+    ax = [a for axes, _ in shards for a in axes]
+    at = [a for _, attrs in shards for a in attrs]
+    naxes, nattr = len(shards[0][0]), len(shards[0][1])
+    ha = (ctypes.c_void_p * len(hs))(*hs)
+    axa = (ctypes.c_void_p * max(1, len(ax)))(*ax)
+    ata = (ctypes.c_void_p * max(1, len(at)))(*at)
+    t = ctypes.c_uint64()
+    check(_lib.bin_execute_group(ha, len(hs), axa, naxes, ata, nattr, ctypes.byref(t)), "bin_execute_group")
+    return t.value
+
+
 def bin_inputs_released(h, ticket):
     ev = ctypes.c_void_p()
     check(_lib.bin_inputs_released(ctypes.c_void_p(h), ticket, ctypes.byref(ev)), "bin_inputs_released")

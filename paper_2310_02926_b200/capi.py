@@ -98,6 +98,9 @@ _SIGS = {
     "bin_execute": (ctypes.c_int, [_vp, _P(_vp), ctypes.c_int32, _P(_vp), ctypes.c_int32, _P(ctypes.c_uint64)]),
     "bin_execute_shards": (ctypes.c_int, [_vp, _P(_vp), ctypes.c_int32, _P(_vp), ctypes.c_int32, ctypes.c_int32,
                                           _P(ctypes.c_uint64)]),
+    "bin_init_group": (ctypes.c_int, [_P(bin_spec_t), _P(bin_placement_t), ctypes.c_int32, _P(_vp)]),
+    "bin_execute_group": (ctypes.c_int, [_P(_vp), ctypes.c_int32, _P(_vp), ctypes.c_int32, _P(_vp), ctypes.c_int32,
+                                         _P(ctypes.c_uint64)]),
     "bin_inputs_released": (ctypes.c_int, [_vp, ctypes.c_uint64, _P(_vp)]),
     "bin_wait": (ctypes.c_int, [_vp, ctypes.c_uint64]),
     "bin_result": (ctypes.c_int, [_vp, ctypes.c_uint64, _P(bin_result_t)]),

@@ -39,6 +39,15 @@ __global__ void __launch_bounds__(COMB_THREADS) k_combine_peer(Geom g, PeerSet p
     combine_peer_body<EXACT>(g, ps, rank, nranks, epoch, meta, variant, bulk != 0);
 }
 
+// One-device rank group (bin_execute_group): rank blockIdx.y runs the same
+// body over its own peer set; the group's ranks all live in this launch.
+template <bool EXACT>
+__global__ void __launch_bounds__(COMB_THREADS) k_combine_group(Geom g, const GroupRank *gr, int nranks,
+                                                                unsigned long long epoch, int variant, int bulk) {
+    const GroupRank &r = gr[blockIdx.y];
+    combine_peer_body<EXACT>(g, r.ps, (int)blockIdx.y, nranks, epoch, r.meta, variant, bulk != 0);
+}
+
 // dynamic shared memory of the bulk slice: NR ranks x 4 words + 5 output words per bin
 static size_t combine_bulk_smem(int nranks) { return ((size_t)nranks * 4 + 5) * COMB_CB * 8; }
 
@@ -68,6 +77,34 @@ cudaError_t launch_combine_peer(const Geom &g, const PeerSet &ps, int rank, int 
     else
         k_combine_peer<false><<<(unsigned)blocks, COMB_THREADS, smem, s>>>(g, ps, rank, nranks, epoch, meta, variant,
                                                                            bulk ? 1 : 0);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_combine_group(const Geom &g, const GroupRank *dev_ranks, const Accum &acc0, int nranks,
+                                 unsigned long long epoch, int variant, int sms, cudaStream_t s) {
+    const uint64_t B = acc0.nbins;
+    const uint64_t slice = (B + nranks - 1) / nranks;
+    static const bool no_bulk = getenv("DATABIN_COMBINE_BULK") && getenv("DATABIN_COMBINE_BULK")[0] == '0';
+    const bool bulk = !no_bulk && !acc0.xs && acc0.nsum <= 1 && acc0.nmm <= 1 &&
+                      (nranks == 2 || nranks == 4 || nranks == 8);
+    // the barriers spin inside this launch: every CTA of every rank must be
+    // resident at once, so at most one CTA per SM in total (<= 75 KB of shared
+    // memory and 256 threads each: any CTA fits an SM on its own)
+    uint64_t per_rank = (uint64_t)(sms / nranks);
+    if (per_rank < 1) per_rank = 1;
+    uint64_t want = bulk ? (slice + COMB_CB - 1) / COMB_CB : (slice * nranks + COMB_THREADS - 1) / COMB_THREADS;
+    const uint64_t blocks = want < 1 ? 1 : (want < per_rank ? want : per_rank);
+    size_t smem = 0;
+    if (bulk) {
+        smem = combine_bulk_smem(nranks);
+        cudaError_t e = cudaFuncSetAttribute(k_combine_group<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    const dim3 grid((unsigned)blocks, (unsigned)nranks);
+    if (acc0.xs)
+        k_combine_group<true><<<grid, COMB_THREADS, 0, s>>>(g, dev_ranks, nranks, epoch, variant, 0);
+    else
+        k_combine_group<false><<<grid, COMB_THREADS, smem, s>>>(g, dev_ranks, nranks, epoch, variant, bulk ? 1 : 0);
     return cudaGetLastError();
 }
 

@@ -195,6 +195,14 @@ struct PeerSet {
 };
 cudaError_t launch_combine_peer(const Geom &g, const PeerSet &ps, int rank, int nranks, unsigned long long epoch,
                                 Meta *meta, int variant, int deterministic, int sms, cudaStream_t s);
+// a rank group on one device: the same combine body for all ranks in one launch
+// (blockIdx.y = rank); every CTA co-resides (<= sms CTAs in total)
+struct GroupRank {
+    PeerSet ps;
+    Meta *meta;
+};
+cudaError_t launch_combine_group(const Geom &g, const GroupRank *dev_ranks, const Accum &acc0, int nranks,
+                                 unsigned long long epoch, int variant, int sms, cudaStream_t s);
 
 // deterministic mode (sort-based, bit-exact vs the sequential oracle)
 struct DetScratch {

@@ -25,6 +25,8 @@ struct Slot {
     PeerSet peers{};
     Meta *meta_h = nullptr, *meta_d = nullptr;
     cudaEvent_t done = nullptr, released = nullptr, zeroed = nullptr;
+    cudaEvent_t binned = nullptr;  // rank group: this rank's accumulate is complete (bin_execute_group)
+    bool staged_any = false;       // rank group: the execute staged inputs (tail deferred to the group)
     bool used_before = false;  // a previous execute used this slot (its done event is valid)
     cudaEvent_t ev[EV_N] = {};
     bool recd[EV_N] = {};  // which events this execute recorded (profiling)
@@ -45,6 +47,19 @@ struct Stage {
 };
 
 }  // namespace
+
+// A rank group on one device (bin_init_group): P handles whose combine is the
+// fused peer combine + finalize over the group's slot arrays, launched once
+// for all P ranks (grid.y = rank) after every rank has binned.
+struct bin_group {
+    int nranks = 0;
+    int device = 0;
+    std::vector<bin_handle *> member;  // rank -> handle (nullptr once finalized)
+    GroupRank *dev = nullptr;          // [2 slots][nranks] peer sets + metas (device)
+    cudaStream_t stream = nullptr;     // the combine's stream
+    cudaEvent_t done[2] = {};
+    int alive = 0;
+};
 
 struct bin_handle {
     bin_spec_t spec{};
@@ -88,6 +103,7 @@ struct bin_handle {
     int64_t wcache_age = 0;
     unsigned char *part_base = nullptr;  // partition-route scratch (grown on demand)
     size_t part_bytes = 0;
+    bin_group *group = nullptr;  // member of a one-device rank group (bin_init_group)
     bool finalized = false;
 };
 
@@ -166,6 +182,8 @@ static void free_slot(bin_handle *h, Slot &s) {
     if (s.released) cudaEventDestroy(s.released);
     if (s.zeroed) cudaEventDestroy(s.zeroed);
     s.zeroed = nullptr;
+    if (s.binned) cudaEventDestroy(s.binned);
+    s.binned = nullptr;
     for (auto &e : s.ev)
         if (e) cudaEventDestroy(e), e = nullptr;
     s.done = s.released = nullptr;
@@ -229,6 +247,7 @@ static int alloc_slot(bin_handle *h, Slot &s) {
     DB_CUDA(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
     DB_CUDA(cudaEventCreateWithFlags(&s.released, cudaEventDisableTiming));
     DB_CUDA(cudaEventCreateWithFlags(&s.zeroed, cudaEventDisableTiming));
+    DB_CUDA(cudaEventCreateWithFlags(&s.binned, cudaEventDisableTiming));
     for (auto &ev : s.ev) DB_CUDA(cudaEventCreate(&ev));
     return BIN_OK;
 }
@@ -557,6 +576,27 @@ static int run_probe(bin_handle *h, const Geom &geom, const Inputs &in, Slot &S,
     return BIN_OK;
 }
 
+// The end of an execute on its work stream S.stream: completion / release
+// events, input-use tracking, and the lockstep wait.
+static int finish_execute(bin_handle *h, Slot &S, bool staged_any, bin_array_t *const *axes, int32_t naxes,
+                          bin_array_t *const *attrs, int32_t nattr, int32_t nshards) {
+    cudaStream_t s = S.stream;
+    DB_CUDA(cudaEventRecord(S.done, s));
+    if (!staged_any) DB_CUDA(cudaEventRecord(S.released, s));
+    S.prof_pending = h->prof;
+    int rc;
+    for (int sh = 0; sh < nshards; ++sh)
+        for (int i = 0; i < naxes + nattr; ++i) {
+            bin_array *a = i < naxes ? axes[sh * naxes + i] : attrs[sh * nattr + i - naxes];
+            if ((rc = array_mark_use(a, s, h->device))) return rc;
+        }
+    if (h->place.exec == BIN_EXEC_SYNC && axes[0]->mode == BIN_SYNC) {
+        cudaError_t e = cudaEventSynchronize(S.done);
+        if (e != cudaSuccess) return cuda_error(e, "bin_execute (lockstep) synchronize");
+    }
+    return BIN_OK;
+}
+
 // One execute over nshards row blocks (nshards == 1: bin_execute).  Shard s's
 // columns are axes[s * ndim + d] and attrs[s * nattr + a].  With several shards
 // every column is staged into one buffer, shard after shard (host: H2D; other
@@ -845,6 +885,13 @@ static int execute_impl(bin_handle *h, bin_array_t *const *axes, int32_t naxes, 
         }
     }
     if ((rc = rec(EV_BIN1, n > 0))) return rc;
+    if (h->group) {  // rank group: bin_execute_group launches the combine once for all ranks
+        DB_CUDA(cudaEventRecord(S.binned, s));
+        S.variant = variant | 32;
+        S.staged_any = staged_any;
+        if (ticket) *ticket = t;
+        return BIN_OK;
+    }
     // ---- a6 + a7 fused over NVLink peer memory (one kernel), or NCCL + finalize
     if (h->peer) {
         if ((e = launch_combine_peer(geom, S.peers, h->rank, h->nranks, t, S.meta_d, variant | 32,
@@ -886,29 +933,19 @@ static int execute_impl(bin_handle *h, bin_array_t *const *axes, int32_t naxes, 
     S.variant = variant;
     if ((rc = rec(EV_FINAL1, true))) return rc;
     }
-    DB_CUDA(cudaEventRecord(S.done, s));
-    if (!staged_any) DB_CUDA(cudaEventRecord(S.released, s));
-    S.prof_pending = h->prof;
-    for (int sh = 0; sh < nshards; ++sh)
-        for (int i = 0; i < ncols; ++i) {
-            bin_array *a = i < naxes ? axes[sh * naxes + i] : attrs[sh * nattr + i - naxes];
-            if ((rc = array_mark_use(a, s, h->device))) return rc;
-        }
     if (ticket) *ticket = t;
-    if (h->place.exec == BIN_EXEC_SYNC && cols[0]->mode == BIN_SYNC) {
-        e = cudaEventSynchronize(S.done);
-        if (e != cudaSuccess) return cuda_error(e, "bin_execute (lockstep) synchronize");
-    }
-    return BIN_OK;
+    return finish_execute(h, S, staged_any, axes, naxes, attrs, nattr, nshards);
 }
 
 int bin_execute(bin_handle_t *h, bin_array_t *const *axes, int32_t naxes, bin_array_t *const *attrs,
                 int32_t nattr, uint64_t *ticket) {
+    if (h && h->group) return set_error(BIN_ESTATE, "bin_execute: handle belongs to a rank group (bin_execute_group)");
     return execute_impl(h, axes, naxes, attrs, nattr, 1, ticket);
 }
 
 int bin_execute_shards(bin_handle_t *h, bin_array_t *const *axes, int32_t naxes, bin_array_t *const *attrs,
                        int32_t nattr, int32_t nshards, uint64_t *ticket) {
+    if (h && h->group) return set_error(BIN_ESTATE, "bin_execute_shards: handle belongs to a rank group");
     return execute_impl(h, axes, naxes, attrs, nattr, nshards, ticket);
 }
 
@@ -1038,6 +1075,150 @@ int bin_result(bin_handle_t *h, uint64_t ticket, bin_result_t *out) {
     return BIN_OK;
 }
 
+// ---------------------------------------------------------------- one-device rank group
+static void group_drop(bin_handle *h) {
+    bin_group *G = h->group;
+    if (!G) return;
+    h->group = nullptr;
+    if (h->rank >= 0 && h->rank < (int)G->member.size() && G->member[h->rank] == h) G->member[h->rank] = nullptr;
+    if (--G->alive > 0) return;
+    DeviceGuard g(G->device);
+    if (G->stream) cudaStreamSynchronize(G->stream), cudaStreamDestroy(G->stream);
+    for (auto &e : G->done)
+        if (e) cudaEventDestroy(e);
+    if (G->dev) cudaFree(G->dev);
+    delete G;
+}
+
+int bin_init_group(const bin_spec_t *spec, const bin_placement_t *place, int32_t nranks, bin_handle_t **out) {
+    if (!spec || !out) return set_error(BIN_EINVAL, "bin_init_group: NULL spec/out");
+    if (nranks < 1 || nranks > PEER_MAX) return set_error(BIN_EINVAL, "bin_init_group: %d ranks (1..%d)", nranks, PEER_MAX);
+    if (spec->bounds_auto)
+        return set_error(BIN_ENOTSUP, "bin_init_group: automatic bounds need the cross-rank Min (NCCL); give manual bounds");
+    for (int r = 0; r < nranks; ++r) out[r] = nullptr;
+    bin_group *G = new bin_group;
+    G->nranks = nranks;
+    G->member.assign(nranks, nullptr);
+    auto fail = [&](int code) {
+        for (int r = 0; r < nranks; ++r)
+            if (out[r]) bin_finalize(out[r]), out[r] = nullptr;
+        if (G->alive == 0) {  // no member took ownership yet
+            if (G->stream) cudaStreamDestroy(G->stream);
+            for (auto &e : G->done)
+                if (e) cudaEventDestroy(e);
+            if (G->dev) cudaFree(G->dev);
+            delete G;
+        }
+        return code;
+    };
+    for (int r = 0; r < nranks; ++r) {
+        int rc = bin_init(spec, place, nullptr, &out[r]);  // one rank each, all on the same device
+        if (rc) return fail(rc);
+    }
+    G->device = out[0]->device;
+    DeviceGuard g(G->device);
+    cudaError_t ce;
+    if ((ce = cudaStreamCreateWithFlags(&G->stream, cudaStreamNonBlocking)) != cudaSuccess)
+        return fail(cuda_error(ce, "bin_init_group: stream"));
+    for (auto &e : G->done)
+        if ((ce = cudaEventCreateWithFlags(&e, cudaEventDisableTiming)) != cudaSuccess)
+            return fail(cuda_error(ce, "bin_init_group: event"));
+    for (int r = 0; r < nranks; ++r) {
+        bin_handle *h = out[r];
+        if ((ce = cudaMalloc(&h->flags, 128 * sizeof(unsigned long long))) != cudaSuccess ||
+            (ce = cudaMemset(h->flags, 0, 128 * sizeof(unsigned long long))) != cudaSuccess ||
+            (ce = cudaMalloc(&h->ctas_done, 64)) != cudaSuccess || (ce = cudaMemset(h->ctas_done, 0, 64)) != cudaSuccess)
+            return fail(cuda_error(ce, "bin_init_group: barrier words"));
+    }
+    std::vector<GroupRank> host((size_t)2 * nranks);
+    for (int k = 0; k < 2; ++k)
+        for (int r = 0; r < nranks; ++r) {
+            bin_handle *h = out[r];
+            PeerSet &ps = h->slot[k].peers;
+            ps = PeerSet{};
+            ps.me = h->slot[k].acc;
+            ps.ctas_done = h->ctas_done + k;
+            ps.ctas_failed = h->ctas_done + 4 + k;
+            for (int p = 0; p < nranks; ++p) {  // same address space: the peers' slot arrays directly
+                const Accum &a = out[p]->slot[k].acc;
+                ps.count[p] = a.count;
+                ps.sum[p] = a.sum;
+                ps.mm[p] = a.mm;
+                ps.omin[p] = a.omin;
+                ps.omax[p] = a.omax;
+                ps.oavg[p] = a.oavg;
+                ps.xs[p] = a.xs;
+                ps.xrange[p] = a.xrange;
+                ps.flags[p] = out[p]->flags;
+            }
+            host[(size_t)k * nranks + r] = GroupRank{ps, h->slot[k].meta_d};
+        }
+    if ((ce = cudaMalloc(&G->dev, host.size() * sizeof(GroupRank))) != cudaSuccess)
+        return fail(cuda_error(ce, "bin_init_group: peer sets"));
+    if ((ce = cudaMemcpy(G->dev, host.data(), host.size() * sizeof(GroupRank), cudaMemcpyHostToDevice)) != cudaSuccess)
+        return fail(cuda_error(ce, "bin_init_group: peer sets"));
+    for (int r = 0; r < nranks; ++r) {
+        out[r]->rank = r;
+        out[r]->nranks = nranks;
+        out[r]->peer = true;
+        out[r]->group = G;
+        G->member[r] = out[r];
+        G->alive++;
+    }
+    return BIN_OK;
+}
+
+int bin_execute_group(bin_handle_t *const *hs, int32_t nranks, bin_array_t *const *axes, int32_t naxes,
+                      bin_array_t *const *attrs, int32_t nattr, uint64_t *ticket) {
+    if (!hs || nranks < 1 || !hs[0] || !hs[0]->group) return set_error(BIN_EINVAL, "bin_execute_group: not a rank group");
+    bin_group *G = hs[0]->group;
+    if (nranks != G->nranks) return set_error(BIN_EINVAL, "bin_execute_group: %d handles for a group of %d", nranks, G->nranks);
+    for (int r = 0; r < nranks; ++r)
+        if (!hs[r] || hs[r]->finalized || hs[r]->group != G || hs[r]->rank != r || G->member[r] != hs[r])
+            return set_error(BIN_ESTATE, "bin_execute_group: handle %d is not rank %d of this group (or finalized)", r, r);
+    if (!axes || (nattr && !attrs)) return set_error(BIN_EINVAL, "bin_execute_group: NULL columns");
+    const uint64_t t = hs[0]->next_ticket;
+    for (int r = 0; r < nranks; ++r)
+        if (hs[r]->next_ticket != t) return set_error(BIN_ESTATE, "bin_execute_group: ranks out of step");
+    // a1-a5 of every rank on its own work stream
+    for (int r = 0; r < nranks; ++r) {
+        uint64_t tr = 0;
+        int rc = execute_impl(hs[r], axes + (size_t)r * naxes, naxes, attrs + (size_t)r * nattr, nattr, 1, &tr);
+        if (rc) return rc;
+    }
+    // a6 + a7: one launch over all ranks once every rank has binned
+    const int sl = (int)(t & 1);
+    DeviceGuard g(G->device);
+    for (int r = 0; r < nranks; ++r) DB_CUDA(cudaStreamWaitEvent(G->stream, hs[r]->slot[sl].binned, 0));
+    bin_handle *h0 = hs[0];
+    Geom geom{};
+    geom.ndim = h0->spec.ndim;
+    geom.bounds_auto = 0;
+    for (int d = 0; d < 3; ++d) {
+        geom.res[d] = d < geom.ndim ? h0->spec.res[d] : 1;
+        geom.lo[d] = d < geom.ndim ? h0->spec.lo[d] : 0.0;
+        geom.hi[d] = d < geom.ndim ? h0->spec.hi[d] : 1.0;
+    }
+    cudaError_t e = launch_combine_group(geom, G->dev + (size_t)sl * nranks, h0->slot[sl].acc, nranks, t,
+                                         h0->slot[sl].variant, h0->lc.sms, G->stream);
+    if (e != cudaSuccess) return cuda_error(e, "group combine kernel");
+    DB_CUDA(cudaEventRecord(G->done[sl], G->stream));
+    for (int r = 0; r < nranks; ++r) {
+        bin_handle *h = hs[r];
+        Slot &S = h->slot[sl];
+        DB_CUDA(cudaStreamWaitEvent(S.stream, G->done[sl], 0));
+        S.launches++;
+        if (h->prof) {
+            DB_CUDA(cudaEventRecord(S.ev[EV_FINAL1], S.stream));
+            S.recd[EV_FINAL1] = true;
+        }
+        int rc = finish_execute(h, S, S.staged_any, axes + (size_t)r * naxes, naxes, attrs + (size_t)r * nattr, nattr, 1);
+        if (rc) return rc;
+    }
+    if (ticket) *ticket = t;
+    return BIN_OK;
+}
+
 int bin_stream(bin_handle_t *h, bin_stream_t *stream) {
     if (!h || !stream) return set_error(BIN_EINVAL, "bin_stream: NULL argument");
     *stream = (bin_stream_t)(h->last ? h->last : h->side);
@@ -1083,6 +1264,7 @@ int bin_finalize(bin_handle_t *h) {
             ncclCommDestroy(h->comm);
             h->comm = nullptr;
         }
+        group_drop(h);
         for (auto &S : h->slot) free_slot(h, S);
         for (auto &row : h->stage)
             for (auto &st : row)
