@@ -125,7 +125,7 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception:  # noqa: BLE001
                 pass
-            time.sleep(0.002)
+            time.sleep(0.0005)
 
     def __exit__(self, *a):
         self.stop.set()
@@ -141,17 +141,35 @@ class ClockSampler:
                 "samples": len(s)}
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def cpu_baseline(w, seconds, rank_rows=None):
-    """The oracle as it stands (single thread), on a bounded sample of the workload."""
+    """The oracle as it stands on a bounded sample of the workload: single-
+    threaded (oracle_databin, P = 1) and in its partition mode with one block
+    per host core (oracle.databin_blocks, P = nproc worker threads; the rank
+    decomposition of PAPER.md:479 run on CPU cores).  ``value`` is the
+    all-core rate; ``single_thread`` the sequential loop's."""
     import numpy as np
 
     import oracle
     import synth
     oracle.build()
 
+    def cols(s, c, threads=0):
+        return ([synth.fill_host(w.dist, w.central, w.seed, synth.COLUMNS[x], s, c, threads) for x in w.axes],
+                [synth.fill_host(w.dist, w.central, w.seed, synth.COLUMNS[x], s, c, threads) for x in w.attrs])
+
     def run(n):
-        axes = [synth.fill_host(w.dist, w.central, w.seed, synth.COLUMNS[c], 0, n) for c in w.axes]
-        attrs = [synth.fill_host(w.dist, w.central, w.seed, synth.COLUMNS[c], 0, n) for c in w.attrs]
+        axes, attrs = cols(0, n)
         t0 = time.perf_counter()
         oracle.databin(axes, attrs, w.res, w.lo, w.hi)
         return time.perf_counter() - t0
@@ -159,16 +177,35 @@ def cpu_baseline(w, seconds, rank_rows=None):
     probe = min(w.n, 2_000_000)
     dt = run(probe)
     rate = probe / dt
-    n = int(min(w.n, max(probe, rate * seconds)))
+    n = int(min(w.n, max(probe, rate * seconds / 2)))
     dt = run(n) if n != probe else dt
-    del np
-    return {"value": n / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"first {n:,} rows of {w.name} (seeded generator), oracle_databin single-threaded, "
-                      f"{dt:.2f} s"}
+    single = {"value": n / dt, "cores": 1, "sample": f"first {n:,} rows of {w.name}, oracle_databin, {dt:.2f} s"}
+    # all cores: partition mode P = nproc over a sample sized to ~seconds/2 of work
+    ncores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    nm = int(min(w.n, max(n, single["value"] * ncores * seconds / 2)))
+    pre = [cols(r * nm // ncores, (r + 1) * nm // ncores - r * nm // ncores) for r in range(ncores)]
+    starts = [r * nm // ncores for r in range(ncores)]
+
+    def rows(s, c):  # pre-generated blocks: the timed part is the oracle alone
+        r = starts.index(s)
+        return pre[r]
+
+    t0 = time.perf_counter()
+    oracle.databin_blocks(rows, nm, w.res, w.lo, w.hi, len(w.attrs), P=ncores, chunk=1 << 62)
+    dtm = time.perf_counter() - t0
+    del np, pre
+    return {"value": nm / dtm, "unit": UNIT, "cores": ncores, "kind": "oracle", "model": cpu_model(),
+            "nproc": os.cpu_count(),
+            "sample": f"first {nm:,} rows of {w.name} (seeded generator, pre-generated), oracle partition mode "
+                      f"P = {ncores} (one block and worker thread per core, grids folded in rank order), "
+                      f"{dtm:.2f} s",
+            "single_thread": single}
 
 
 def reference_arm(args):
-    """--impl reference: the oracle (this tier's reference), timed on host cores."""
+    """--impl reference: the oracle (this tier's reference), timed on the host
+    cores: its partition mode with one block and worker thread per core
+    (oracle.databin_blocks, P = cores) on a bounded sample per step."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
@@ -177,25 +214,43 @@ def reference_arm(args):
     import oracle
     oracle.build()
     per_step = max(0.25, args.cpu_seconds / max(1, args.steps + args.warmup))  # K+W steps in ~a minute
-    probe = cpu_baseline(w, per_step)
-    n = int(probe["value"] * per_step)
-    n = max(100_000, min(n, w.n))
-    axes = [synth.fill_host(w.dist, w.central, w.seed, synth.COLUMNS[c], 0, n) for c in w.axes]
-    attrs = [synth.fill_host(w.dist, w.central, w.seed, synth.COLUMNS[c], 0, n) for c in w.attrs]
+    ncores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+
+    def cols(s, c):
+        return ([synth.fill_host(w.dist, w.central, w.seed, synth.COLUMNS[x], s, c) for x in w.axes],
+                [synth.fill_host(w.dist, w.central, w.seed, synth.COLUMNS[x], s, c) for x in w.attrs])
+
+    probe_n = min(w.n, 1_000_000)
+    pax, pat = cols(0, probe_n)
+    t0 = time.perf_counter()
+    oracle.databin(pax, pat, w.res, w.lo, w.hi)
+    rate1 = probe_n / (time.perf_counter() - t0)
+    n = max(100_000, min(int(rate1 * ncores * per_step), w.n))
+    starts = [r * n // ncores for r in range(ncores)]
+    pre = [cols(starts[r], (r + 1) * n // ncores - starts[r]) for r in range(ncores)]
+
+    def rows(s, c):
+        return pre[starts.index(s)]
+
+    def step():
+        oracle.databin_blocks(rows, n, w.res, w.lo, w.hi, len(w.attrs), P=ncores, chunk=1 << 62)
+
     for _ in range(args.warmup):
-        oracle.databin(axes, attrs, w.res, w.lo, w.hi)
+        step()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        oracle.databin(axes, attrs, w.res, w.lo, w.hi)
+        step()
     dt = (time.perf_counter() - t0) / max(1, args.steps)
     v = n / dt
+    sample = (f"first {n:,} rows of {w.name} per step (pre-generated), C oracle in partition mode P = {ncores} "
+              f"(one block and worker thread per core)")
     line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
             "config": {"workload": w.name, "rows_per_step": n, "res": list(w.res), "attrs": list(w.attrs),
                        "ops": list(w.ops)},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": f"first {n:,} rows of {w.name} per step, single-threaded C oracle"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": ncores, "kind": "oracle", "model": cpu_model(),
+                             "sample": sample, "single_thread_probe": rate1},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 

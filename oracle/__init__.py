@@ -55,6 +55,19 @@ def _load():
             lib.oracle_exact_sums.argtypes = [ctypes.c_int, i32_p, d_p, d_p, ctypes.c_int64, dpp, ctypes.c_int,
                                               dpp, d_p]
             lib.oracle_exact_sums.restype = ctypes.c_int
+            u64p = P(ctypes.c_uint64)
+            lib.oracle_grid_init.argtypes = [ctypes.c_int64, ctypes.c_int, u64p, d_p, d_p, d_p, d_p]
+            lib.oracle_grid_init.restype = None
+            lib.oracle_accumulate.argtypes = [ctypes.c_int, i32_p, d_p, d_p, ctypes.c_int64, dpp, ctypes.c_int, dpp,
+                                              u64p, d_p, d_p, d_p, d_p, u64p, u64p]
+            lib.oracle_accumulate.restype = None
+            lib.oracle_merge_into.argtypes = [ctypes.c_int64, ctypes.c_int, u64p, d_p, d_p, d_p, d_p,
+                                              u64p, d_p, d_p, d_p, d_p]
+            lib.oracle_merge_into.restype = None
+            lib.oracle_finalize.argtypes = [ctypes.c_int64, ctypes.c_int, u64p, d_p, d_p]
+            lib.oracle_finalize.restype = None
+            lib.oracle_bounds_usable.argtypes = [ctypes.c_int, i32_p, d_p, d_p]
+            lib.oracle_bounds_usable.restype = ctypes.c_int
             lib.oracle_eq1_device.argtypes = [ctypes.c_int] * 5
             lib.oracle_eq1_device.restype = ctypes.c_int
             _lib = lib
@@ -142,6 +155,72 @@ def databin(axes, attrs, res, lo=None, hi=None, bounds_auto=False, P=1, exact=Fa
         with np.errstate(invalid="ignore", divide="ignore"):
             out["avg_exact"] = np.where(count > 0, se[k] / np.maximum(count, 1).astype(np.float64), np.nan)
     return out
+
+
+def databin_blocks(rows, n, res, lo, hi, nattr, P=1, threads=None, chunk=1 << 24):
+    """The partition mode of ``databin`` for inputs too large to
+    hold at once: ``rows(start, count) -> (axes, attrs)`` produces the columns
+    of rows [start, start + count) (e.g. the seeded generator).  Block r of P
+    = [floor(rN/P), floor((r+1)N/P)) is fed to ``oracle_accumulate`` chunk by
+    chunk in row order into its own grid (one worker thread per block; the C
+    call releases the GIL), then the grids are folded in rank order with
+    ``oracle_merge_into`` and finished with ``oracle_finalize`` -- the C
+    definition of ``oracle_databin(..., P)`` step for step, so the result is
+    bit-identical to ``databin(axes, attrs, res, lo, hi, P=P)``.  P = 1 is the
+    sequential row-order loop.  Manual bounds only.  Same keys as ``databin``
+    (without ``sum_exact``)."""
+    from concurrent.futures import ThreadPoolExecutor
+    lib = _load()
+    ndim = len(res)
+    resa = np.ascontiguousarray(res, dtype=np.int32)
+    B = int(np.prod(resa.astype(np.int64)))
+    loa = np.zeros(3, np.float64)
+    hia = np.zeros(3, np.float64)
+    loa[:ndim] = lo
+    hia[:ndim] = hi
+    rp = resa.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+    if not lib.oracle_bounds_usable(ndim, rp, _dptr(loa), _dptr(hia)):
+        raise InvalidArgument("unusable manual bounds (reading R4)")
+    A = max(nattr, 1)
+    u64 = lambda a: a.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64))  # noqa: E731
+
+    def grid():
+        g = dict(count=np.empty(B, np.uint64), sum=np.empty((A, B)), sumabs=np.empty((A, B)),
+                 min=np.empty((A, B)), max=np.empty((A, B)), n_in=ctypes.c_uint64(0), n_out=ctypes.c_uint64(0))
+        lib.oracle_grid_init(B, nattr, u64(g["count"]), _dptr(g["sum"]), _dptr(g["sumabs"]), _dptr(g["min"]),
+                             _dptr(g["max"]))
+        return g
+
+    def block(r):
+        g = grid()
+        b0, b1 = r * n // P, (r + 1) * n // P
+        for s0 in range(b0, b1, chunk):
+            c = min(chunk, b1 - s0)
+            axes, attrs = rows(s0, c)
+            axes, attrs = _as_f64(axes, c), _as_f64(attrs, c)
+            lib.oracle_accumulate(ndim, rp, _dptr(loa), _dptr(hia), c, _ptr_array(axes), nattr, _ptr_array(attrs),
+                                  u64(g["count"]), _dptr(g["sum"]), _dptr(g["sumabs"]), _dptr(g["min"]),
+                                  _dptr(g["max"]), ctypes.byref(g["n_in"]), ctypes.byref(g["n_out"]))
+        return g
+
+    with ThreadPoolExecutor(max_workers=threads or P) as ex:
+        parts = list(ex.map(block, range(P)))
+    if P == 1:
+        out = parts[0]
+    else:
+        out = grid()
+        for g in parts:  # rank order
+            lib.oracle_merge_into(B, nattr, u64(out["count"]), _dptr(out["sum"]), _dptr(out["sumabs"]),
+                                  _dptr(out["min"]), _dptr(out["max"]), u64(g["count"]), _dptr(g["sum"]),
+                                  _dptr(g["sumabs"]), _dptr(g["min"]), _dptr(g["max"]))
+            out["n_in"].value += g["n_in"].value
+            out["n_out"].value += g["n_out"].value
+    avg = np.empty((A, B))
+    lib.oracle_finalize(B, nattr, u64(out["count"]), _dptr(out["sum"]), _dptr(avg))
+    k = slice(0, nattr)
+    return dict(count=out["count"], sum=out["sum"][k], sumabs=out["sumabs"][k], min=out["min"][k],
+                max=out["max"][k], avg=avg[k], n_in=int(out["n_in"].value), n_out=int(out["n_out"].value),
+                lo=loa[:ndim].copy(), hi=hia[:ndim].copy())
 
 
 def exact_sum(values) -> float:

@@ -143,3 +143,50 @@ def test_window_route_forced_on_uniform(db):
     out = run_gpu(db, axes, attrs, (512, 512), (-1, -1), (1, 1), route="window")
     assert out["profile"].variant & 15 == 1
     compare(out, ref)
+
+
+# ---------------------------------------------------------------- full size (BASELINE.json configs[3])
+@pytest.mark.slow
+def test_c4_full_1B_256cube(db):
+    """C4 at its full 1B rows on one B200 in the bench's launch configuration
+    (auto route -> partition route, two-level grouping into thousands of
+    tiles, 64-bit row offsets), every one of the 16.7M bins compared with the
+    oracle.  The oracle streams the seeded rows chunk by chunk in partition
+    mode P (``oracle.databin_blocks`` is bit-identical to
+    ``oracle.databin(..., P)``), P worker threads on the host cores:
+    counts/min/max bit-exact, sums within reading R8."""
+    import os
+
+    import torch
+    w = synth.CONFIGS["c4"]
+    dev = torch.device("cuda:0")
+    names = list(w.axes) + list(w.attrs)
+    cols = [torch.empty(w.n, dtype=torch.float64, device=dev) for _ in names]
+    st = torch.cuda.current_stream(dev).cuda_stream
+    for t, c in zip(cols, names):
+        synth.fill_device(w.dist, w.central, w.seed, synth.COLUMNS[c], 0, w.n, t.data_ptr(), st)
+    torch.cuda.synchronize(dev)
+    hs = [db.wrap_tensor(t) for t in cols]
+    spec = db.make_spec(w.res, w.lo, w.hi, nattr=len(w.attrs))
+    h = db.bin_init(spec, db.make_placement(device_id=0))
+    try:
+        db.bin_profile_enable(h, True)
+        t = db.bin_execute(h, hs[:3], hs[3:])
+        out = db.result_to_numpy(h, t, spec)
+        variant = db.bin_profile_read(h).variant
+    finally:
+        db.bin_finalize(h)
+        for a in hs:
+            db.bin_array_release(a)
+        del cols
+        torch.cuda.empty_cache()
+    assert variant & 15 == 4, variant                      # the partition route, as bench.py --workload c4 runs it
+
+    def rows(s, c):
+        return ([synth.fill_host(w.dist, w.central, w.seed, synth.COLUMNS[x], s, c, 1) for x in w.axes],
+                [synth.fill_host(w.dist, w.central, w.seed, synth.COLUMNS[x], s, c, 1) for x in w.attrs])
+
+    P = max(1, min(os.cpu_count() or 1, 24))
+    ref = oracle.databin_blocks(rows, w.n, w.res, w.lo, w.hi, len(w.attrs), P=P)
+    assert ref["n_in"] == w.n and ref["n_out"] == 0
+    compare(out, ref)

@@ -396,3 +396,26 @@ def test_manual_bounds_must_be_usable():
     assert r["count"].tolist() == [1, 2]
     r = oracle.databin([[0.0, 1e-300]], [[1.0, 2.0]], [2], [0.0], [1e-300])
     assert r["count"].tolist() == [1, 1]
+
+
+# ---------------------------------------------------------------- streamed partition mode
+@pytest.mark.parametrize("P", [1, 2, 5])
+def test_databin_blocks_is_partition_mode(P):
+    """oracle.databin_blocks (the streamed form used for the 1B-row C4 check)
+    is the partition mode of oracle_databin step for step: bit-identical in
+    every output for any chunking, including chunks that split blocks."""
+    import synth
+    w = synth.CONFIGS["c4"]
+    n = 300_007
+
+    def rows(s, c):
+        return ([synth.fill_host(w.dist, w.central, w.seed, synth.COLUMNS[x], s, c) for x in w.axes],
+                [synth.fill_host(w.dist, w.central, w.seed, synth.COLUMNS[x], s, c) for x in ("mass", "vx")])
+
+    axes, attrs = rows(0, n)
+    ref = oracle.databin(axes, attrs, [16, 8, 4], [-1, -1, -1], [1, 1, 0.5], P=P)
+    got = oracle.databin_blocks(rows, n, [16, 8, 4], [-1, -1, -1], [1, 1, 0.5], 2, P=P, chunk=65_537)
+    for k in ("count", "sum", "sumabs", "min", "max", "avg"):
+        assert np.array_equal(np.asarray(ref[k]).view(np.uint64), np.asarray(got[k]).view(np.uint64)), k
+    assert (ref["n_in"], ref["n_out"]) == (got["n_in"], got["n_out"])
+    assert got["n_out"] > 0
