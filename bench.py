@@ -52,6 +52,8 @@ def parse():
     p.add_argument("--deterministic", action="store_true")
     p.add_argument("--exact", action="store_true", help="BIN_SUM_EXACT: correctly rounded exact sums (R20)")
     p.add_argument("--rows", type=int, default=0, help="experiments only: override the workload's total rows")
+    p.add_argument("--ops", default="", help="experiments only: comma list of ops instead of the workload's "
+                                             "('none' = count only)")
     return p.parse_args()
 
 
@@ -276,6 +278,10 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     w = synth.CONFIGS[args.workload]
+    if args.ops:
+        import dataclasses
+        w = dataclasses.replace(w, ops=tuple(o for o in args.ops.split(",") if o != "none"),
+                                attrs=w.attrs if args.ops != "none" else ())
     N_total = (args.rows or w.n) * (world if args.scaling == "weak" else 1)
     r0, r1 = shard(N_total, rank, world)
     n = r1 - r0

@@ -3,15 +3,17 @@
 // C4, C5 and the paper's Fig. 1 sum-of-mass), same window layout and
 // arithmetic as k_bin (bin_general.cu), written for few instructions per row:
 //
-//  * 32-bit pair indices, shared memory addressed as one u32 array with
-//    warp-uniform word offsets (no generic-pointer round trips);
+//  * 32-bit pair indices, shared memory addressed as one u32 array through
+//    32-bit shared-window addresses from one base register;
 //  * one 16-byte pair per column prefetched one step ahead in registers;
-//  * a per-warp queue of rare work.  Rows outside the window (~8% on C3) and
-//    min/max candidates inside it (~12%: a CTA-bin sees only ~80 rows, so its
-//    running extremes still move) would otherwise be divergent branches that
-//    nearly every warp takes.  Lanes append (kind | bin, value) with a ballot
-//    and the warp executes 32 queued items at a time with every lane busy,
-//    as fire-and-forget L2 reductions (REDG.ADD / REDG.MIN, no loads).
+//  * every row's work issued by its own lane: shared-memory count, 96-bit
+//    fixed-point sum and min/max filter for rows in the CTA's window, and
+//    predicated fire-and-forget L2 reductions for the rare work (rows outside
+//    the window, min/max candidates, values outside the fixed-point range).
+//    Round 1 batched that rare work through a per-warp queue drained 32 items
+//    at a time; the pushes cost ~40 issue slots per row pair and the queue
+//    ~24 KB of window, and the direct form measured 0.575 vs 0.591 ms on C3
+//    (profiles/r02_kbin_ablation.txt).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -27,19 +29,15 @@ extern __shared__ __align__(16) uint32_t f_dsm[];
 #define BIN_FAST_THREADS 1024
 #endif
 constexpr int FAST_THREADS = BIN_FAST_THREADS;
-constexpr int QCAP = 64;            // >= 31 leftover + 32 new items
-constexpr int QWORDS = 3 * QCAP;    // u32 tags[QCAP] + f64 vals[QCAP]
-constexpr uint32_t QBIN = (1u << 29) - 1;
-enum : uint32_t { QK_GLOBAL = 1u, QK_MIN = 2u, QK_MAX = 4u };
+// Shared memory past the window: none beyond alignment slack.
+int fast_queue_bytes() { return 16; }
 
-int fast_queue_bytes() { return (FAST_THREADS / 32) * QWORDS * 4 + 16; }
+// Window bytes per bin: count u32, fixed-point sum 3 x u32, min/max filter
+// 2 x u32.  (Exact u64 min/max in the window instead of the filter -- 32 B per
+// bin, an LDS.128 per row -- measured 0.637 vs 0.591 ms on C3: the smaller
+// window sent more rows to L2.)
+int fast_window_bytes_per_bin(const Accum &acc) { return 4 + 12 * acc.nsum + 8 * acc.nmm; }
 
-// Shared-memory window accesses through 32-bit shared-window addresses from one
-// base register (BIN_SADDR=1): generic atomics on the extern array made the
-// compiler re-derive the window base (S2R SR_CgaCtaId + LEA) for every row.
-#ifndef BIN_SADDR
-#define BIN_SADDR 1
-#endif
 __device__ __forceinline__ void s_red_add(uint32_t a, uint32_t v) {
     asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a), "r"(v));
 }
@@ -63,11 +61,49 @@ struct FastCtx {
     FxParam fx;
     uint32_t o_fx, o_cnt;  // word offsets (filters at 0)
     uint32_t sb;           // shared-window address of f_dsm[0]
+    unsigned long long *mm;  // global {enc(min), ~enc(max)} slots
 };
 
+struct FastX {
+    long long *xs;  // nullptr: BIN_SUM_FAST
+    uint64_t B;
+    int *sxr;       // this CTA's touched digit range (shared memory)
+};
+
+// ---- predicated fire-and-forget reductions (no branch region per row) ----
+__device__ __forceinline__ void ps_add(bool p, uint32_t a, uint32_t v) {
+    asm volatile("{ .reg .pred q; setp.ne.b32 q, %0, 0; @q red.shared.add.u32 [%1], %2; }" ::"r"((int)p), "r"(a), "r"(v)
+                 : "memory");
+}
+__device__ __forceinline__ void ps_min(bool p, uint32_t a, uint32_t v) {
+    asm volatile("{ .reg .pred q; setp.ne.b32 q, %0, 0; @q red.shared.min.u32 [%1], %2; }" ::"r"((int)p), "r"(a), "r"(v)
+                 : "memory");
+}
+__device__ __forceinline__ void pg_add_u64(bool p, unsigned long long *a, unsigned long long v) {
+    asm volatile("{ .reg .pred q; setp.ne.b32 q, %0, 0; @q red.relaxed.gpu.global.add.u64 [%1], %2; }" ::"r"((int)p),
+                 "l"(a), "l"(v) : "memory");
+}
+__device__ __forceinline__ void pg_add_f64(bool p, double *a, double v) {
+    asm volatile("{ .reg .pred q; setp.ne.b32 q, %0, 0; @q red.relaxed.gpu.global.add.f64 [%1], %2; }" ::"r"((int)p),
+                 "l"(a), "d"(v) : "memory");
+}
+__device__ __forceinline__ void pg_min_u64(bool p, unsigned long long *a, unsigned long long v) {
+    asm volatile("{ .reg .pred q; setp.ne.b32 q, %0, 0; @q red.relaxed.gpu.global.min.u64 [%1], %2; }" ::"r"((int)p),
+                 "l"(a), "l"(v) : "memory");
+}
+
+// One row, all of its work issued by its own lane: in
+// the window -> shared-memory count, 96-bit fixed-point sum and the min/max
+// filter (an improving row also sends its exact value to the global slot);
+// outside it -> L2 reductions of count, sum, min and max.  A value outside the
+// fixed-point range sends its sum to L2 (its count and min/max stay in the
+// window).  sm_100a ptxas wraps every predicated atomic in its own BSSY/BRA/
+// BSYNC region; grouping the rare ones into fewer regions (with min-with-~0
+// no-ops for the half not needed) was measured slower: 0.651 vs 0.583 ms on
+// C3 -- the no-op reductions cost more than the regions.
 template <int D, int A, int SM, int MM, bool XS>
-__device__ __forceinline__ uint32_t fast_row(const FastCtx<D> &c, const double (&x)[D], double v, bool valid,
-                                             uint32_t &n_in) {
+__device__ __forceinline__ void lean_row(const FastCtx<D> &c, const double (&x)[D], double v, bool valid,
+                                         uint32_t &n_in, unsigned long long *count, double *sum, const FastX &X) {
     constexpr bool HS = A == 1 && SM == 1, HM = A == 1 && MM == 1;
     bool ok = valid;
     int k[D];
@@ -76,9 +112,8 @@ __device__ __forceinline__ uint32_t fast_row(const FastCtx<D> &c, const double (
         ok = ok && (c.lo[d] <= x[d]) && (x[d] <= c.hi[d]);
         k[d] = min(floor_nonneg(__dmul_rn(__dsub_rn(x[d], c.lo[d]), c.scale[d])), c.resm1[d]);
     }
-    if (!ok) return 0u;
-    ++n_in;
-    bool inw = true;
+    n_in += ok ? 1u : 0u;
+    bool inw = ok;
     uint32_t l = 0;
 #pragma unroll
     for (int d = D - 1; d >= 0; --d) {
@@ -89,134 +124,51 @@ __device__ __forceinline__ uint32_t fast_row(const FastCtx<D> &c, const double (
     uint32_t b = (uint32_t)k[0];
     if (D >= 2) b += (uint32_t)(c.resm1[0] + 1) * (uint32_t)k[1];
     if (D >= 3) b += (uint32_t)(c.resm1[0] + 1) * (uint32_t)(c.resm1[D > 2 ? 1 : 0] + 1) * (uint32_t)k[D > 2 ? 2 : 0];
-    if (!inw) return (QK_GLOBAL << 29) | b;
-    if (BIN_SADDR) s_red_add(c.sb + 4u * (c.o_cnt + l), 1u);
-    else atomicAdd(&f_dsm[c.o_cnt + l], 1u);
+    const bool glob = ok && !inw;
     const uint32_t W = c.W;
-    uint32_t tag = 0;
+    ps_add(inw, c.sb + 4u * (c.o_cnt + l), 1u);
+    bool sum_glob = glob;
     if (HS) {
-        const uint32_t w0 = c.o_fx + l;
-        unsigned qmid;
+        const uint32_t a0 = c.sb + 4u * (c.o_fx + l);
         unsigned long long q = 0;
         bool fx;
         if (XS) {
             fx = fx_quant_exact(c.fx, v, q);
         } else {
             fx = fx_path(c.fx, v);
-            if (fx) q = fx_quant(c.fx, v);
+            q = fx ? fx_quant(c.fx, v) : 0ull;
         }
-        if (fx) {
+        fx = fx && inw;
+        sum_glob = glob || (inw && !fx);
+        if (inw) {  // (almost every lane: a short region)
+            if (!fx) q = (unsigned long long)FX_OFFSET;  // count-only offset: the sum goes to L2
             const unsigned qlo = (unsigned)q;
-            qmid = (unsigned)(q >> 32);
-            const unsigned old = BIN_SADDR ? s_atom_add(c.sb + 4u * w0, qlo) : atomicAdd(&f_dsm[w0], qlo);
+            unsigned qmid = (unsigned)(q >> 32);
+            const unsigned old = s_atom_add(a0, qlo);
             qmid += (old + qlo < old) ? 1u : 0u;
-        } else {  // rare: outside the fixed range -> sum (and min/max) go global; count stays here
-            tag = ((QK_GLOBAL | QK_MIN) << 29) | b;
-            qmid = FX_OFFSET_MID;
-        }
-        const unsigned old2 = BIN_SADDR ? s_atom_add(c.sb + 4u * (w0 + W), qmid) : atomicAdd(&f_dsm[w0 + W], qmid);
-        if (old2 + qmid < old2) {
-            if (BIN_SADDR) s_red_add(c.sb + 4u * (w0 + 2 * W), 1u);
-            else atomicAdd(&f_dsm[w0 + 2 * W], 1u);
+            const unsigned old2 = s_atom_add(a0 + 4u * W, qmid);
+            ps_add(old2 + qmid < old2, a0 + 8u * W, 1u);  // rare carry into the high word
         }
     }
-    if (HM && tag == 0) {
+    if (HM) {
         const unsigned long long e = enc_total(v);
         const unsigned eh = (unsigned)(e >> 32), neh = ~eh;
-        uint2 f;  // one LDS.64; stale values are safe (the words only decrease)
-        const uint32_t fa = BIN_SADDR ? c.sb + 8u * l : (unsigned)__cvta_generic_to_shared(&f_dsm[2 * l]);
-        asm volatile("ld.volatile.shared.v2.u32 {%0, %1}, [%2];" : "=r"(f.x), "=r"(f.y) : "r"(fa));
-        uint32_t kind = 0;
-        if (eh <= f.x) {
-            kind |= QK_MIN;
-            if (eh < f.x) {
-                if (BIN_SADDR) s_red_min(fa, eh);
-                else atomicMin(&f_dsm[2 * l], eh);
-            }
-        }
-        if (neh <= f.y) {
-            kind |= QK_MAX;
-            if (neh < f.y) {
-                if (BIN_SADDR) s_red_min(fa + 4u, neh);
-                else atomicMin(&f_dsm[2 * l + 1], neh);
-            }
-        }
-        if (kind) tag = (kind << 29) | b;
+        uint2 f = make_uint2(0u, 0u);  // (a row outside the window: the filter does not apply)
+        const uint32_t fa = c.sb + 8u * l;
+        if (inw) asm volatile("ld.volatile.shared.v2.u32 {%0, %1}, [%2];" : "=r"(f.x), "=r"(f.y) : "r"(fa));
+        ps_min(inw && eh < f.x, fa, eh);
+        ps_min(inw && neh < f.y, fa + 4u, neh);
+        unsigned long long *g = c.mm + 2ull * b;
+        pg_min_u64(glob || (inw && eh <= f.x), g, e);
+        pg_min_u64(glob || (inw && neh <= f.y), g + 1, ~e);
     }
-    return tag;
-}
-
-// One queued item as fire-and-forget L2 reductions.  A QK_GLOBAL item from
-// inside the window (value outside the fixed range) carries sum + min/max but
-// its count is already in shared memory -> the low bit of `kind` picks count.
-// `gf` (the CTA's window covers under half its rows, e.g. uniform data): the
-// global rows' min/max first read the slot pair from L2 and reduce only when
-// they improve it (stale reads are safe: the slots only decrease), which turns
-// two L2 atomics per global row into one load for all but the first rows.
-// Exact sums (BIN_SUM_EXACT): digit rows instead of the f64 reduction.
-struct FastX {
-    long long *xs;  // nullptr: BIN_SUM_FAST
-    uint64_t B;
-    int *sxr;       // this CTA's touched digit range (shared memory)
-};
-
-template <int A, int SM, int MM, bool XS>
-__device__ __forceinline__ void fast_exec(uint32_t tag, double v, unsigned long long *count, double *sum,
-                                          ulonglong2 *mm, bool gf, const FastX &X) {
-    constexpr bool HS = A == 1 && SM == 1, HM = A == 1 && MM == 1;
-    const uint32_t kind = tag >> 29, b = tag & QBIN;
-    if (kind & QK_GLOBAL) {
-        if (!(kind & QK_MIN)) atomicAdd(&count[b], 1ull);  // QK_GLOBAL|QK_MIN marks "count already counted"
-        if (HS) {
-            if (XS) xsum_add_double(X.xs, X.B, 0, b, v, X.sxr);
-            else atomicAdd(&sum[b], v);
+    pg_add_u64(glob, count + b, 1ull);
+    if (HS) {
+        if (XS) {
+            if (sum_glob) xsum_add_double(X.xs, X.B, 0, b, v, X.sxr);
+        } else {
+            pg_add_f64(sum_glob, sum + b, v);
         }
-        if (HM) {
-            const unsigned long long e = enc_total(v);
-            ulonglong2 cur = make_ulonglong2(~0ull, ~0ull);
-            if (gf) cur = __ldcg(&mm[b]);
-            if (e < cur.x) atomicMin(&mm[b].x, e);
-            if (~e < cur.y) atomicMin(&mm[b].y, ~e);
-        }
-    } else if (HM) {
-        const unsigned long long e = enc_total(v);
-        if (kind & QK_MIN) atomicMin(&mm[b].x, e);
-        if (kind & QK_MAX) atomicMin(&mm[b].y, ~e);
-    }
-}
-
-template <int A, int SM, int MM, bool XS>
-__device__ __forceinline__ void fast_push(uint32_t qb, uint32_t &qn, uint32_t tag, double v, unsigned lane,
-                                          unsigned long long *count, double *sum, ulonglong2 *mm, bool gf,
-                                          const FastX &X) {
-    const unsigned m = __ballot_sync(0xffffffffu, tag != 0);
-    if (m == 0) return;
-    double *vals = (double *)&f_dsm[qb + QCAP];
-    if (tag) {
-        const unsigned pos = qn + __popc(m & ((1u << lane) - 1u));
-        f_dsm[qb + pos] = tag;
-        vals[pos] = v;
-    }
-    qn += __popc(m);
-    if (qn >= 32) {
-        __syncwarp();
-        const uint32_t t = f_dsm[qb + lane];
-        const double vv = vals[lane];
-        const unsigned rest = qn - 32;
-        uint32_t t2 = 0;
-        double v2 = 0.0;
-        if (lane < rest) {
-            t2 = f_dsm[qb + 32 + lane];
-            v2 = vals[32 + lane];
-        }
-        __syncwarp();
-        if (lane < rest) {
-            f_dsm[qb + lane] = t2;
-            vals[lane] = v2;
-        }
-        qn = rest;
-        fast_exec<A, SM, MM, XS>(t, vv, count, sum, mm, gf, X);
-        __syncwarp();
     }
 }
 
@@ -308,7 +260,6 @@ __global__ void __launch_bounds__(FAST_THREADS, 1)
     FastCtx<D> c;
     unsigned long long *const count = acc.count;
     double *const sum = acc.sum;
-    ulonglong2 *const mm = (ulonglong2 *)acc.mm;
 
     const double2 *cx[D];
 #pragma unroll
@@ -356,11 +307,7 @@ __global__ void __launch_bounds__(FAST_THREADS, 1)
         }
     }
     c.fx = XS ? fx_param_exact(s_exp) : fx_param(HS ? s_exp : 0u);
-#ifdef BIN_GF_OFF
-    const bool gf = false;
-#else
-    const bool gf = s_origin[3] != 0;
-#endif
+    c.mm = acc.mm;
     double2 bx[D], bv = make_double2(0.0, 0.0);
     if (p0 < npairs) {
 #pragma unroll
@@ -379,36 +326,47 @@ __global__ void __launch_bounds__(FAST_THREADS, 1)
     const uint32_t o_end = c.o_cnt + W;
     for (uint32_t i = c.o_fx + threadIdx.x; i < o_end; i += FAST_THREADS) f_dsm[i] = 0u;
     const unsigned lane = threadIdx.x & 31u;
-    const uint32_t qb = ((o_end + 3u) & ~3u) + (threadIdx.x >> 5) * QWORDS;
     const FastX X{XS ? acc.xs : nullptr, acc.nbins, s_xr};
-    uint32_t qn = 0;
     __syncthreads();
 
     trace(1);
     uint32_t n_in = 0, rows = 0;
-    for (uint32_t pb = p0 - lane; pb < npairs; pb += nthr) {  // warp-uniform trip count
-        const uint32_t pc = pb + lane;
-        const bool valid = pc < npairs;
-        const uint32_t pn = pc + nthr;
-        double2 nx[D], nv = make_double2(0.0, 0.0);
-        if (pn < npairs) {
+    {
+        for (uint32_t pb = p0 - lane; pb < npairs; pb += nthr) {  // warp-uniform trip count
+            const uint32_t pc = pb + lane;
+            const bool valid = pc < npairs;
+            const uint32_t pn = pc + nthr;
+            double2 nx[D], nv = make_double2(0.0, 0.0);
+            if (pn < npairs) {
 #pragma unroll
-            for (int d = 0; d < D; ++d) nx[d] = __ldcs(cx[d] + pn);
-            if (A == 1) nv = __ldcs(cv + pn);
+                for (int d = 0; d < D; ++d) nx[d] = __ldcs(cx[d] + pn);
+                if (A == 1) nv = __ldcs(cv + pn);
+            }
+#ifdef BIN_FAST_LOADS_ONLY  // experiment: the streaming floor of this loop (rows consumed, nothing binned)
+            {
+                double acc_ = bv.x + bv.y;
+#pragma unroll
+                for (int d = 0; d < D; ++d) acc_ += bx[d].x + bx[d].y;
+                n_in += (valid && acc_ == 12345.678) ? 1u : 0u;
+                rows += valid ? 2u : 0u;
+#pragma unroll
+                for (int d = 0; d < D; ++d) bx[d] = nx[d];
+                bv = nv;
+                continue;
+            }
+#endif
+            double x[D];
+#pragma unroll
+            for (int d = 0; d < D; ++d) x[d] = bx[d].x;
+            lean_row<D, A, SM, MM, XS>(c, x, bv.x, valid, n_in, count, sum, X);
+#pragma unroll
+            for (int d = 0; d < D; ++d) x[d] = bx[d].y;
+            lean_row<D, A, SM, MM, XS>(c, x, bv.y, valid, n_in, count, sum, X);
+            rows += valid ? 2u : 0u;
+#pragma unroll
+            for (int d = 0; d < D; ++d) bx[d] = nx[d];
+            bv = nv;
         }
-        double x[D];
-#pragma unroll
-        for (int d = 0; d < D; ++d) x[d] = bx[d].x;
-        uint32_t t0 = fast_row<D, A, SM, MM, XS>(c, x, bv.x, valid, n_in);
-        fast_push<A, SM, MM, XS>(qb, qn, t0, bv.x, lane, count, sum, mm, gf, X);
-#pragma unroll
-        for (int d = 0; d < D; ++d) x[d] = bx[d].y;
-        uint32_t t1 = fast_row<D, A, SM, MM, XS>(c, x, bv.y, valid, n_in);
-        fast_push<A, SM, MM, XS>(qb, qn, t1, bv.y, lane, count, sum, mm, gf, X);
-        rows += valid ? 2u : 0u;
-#pragma unroll
-        for (int d = 0; d < D; ++d) bx[d] = nx[d];
-        bv = nv;
     }
     // the unpaired head row (lane 0) and tail row (lane 1) of the whole input, on warp 0 of CTA 0
     if (blockIdx.x == 0 && threadIdx.x < 32) {
@@ -418,13 +376,9 @@ __global__ void __launch_bounds__(FAST_THREADS, 1)
 #pragma unroll
         for (int d = 0; d < D; ++d) x[d] = r >= 0 ? in.ax[d][r] : 0.0;
         if (A == 1 && r >= 0) v = in.at[0][r];
-        const uint32_t t = fast_row<D, A, SM, MM, XS>(c, x, v, r >= 0, n_in);
+        lean_row<D, A, SM, MM, XS>(c, x, v, r >= 0, n_in, count, sum, X);
         rows += r >= 0 ? 1u : 0u;
-        fast_push<A, SM, MM, XS>(qb, qn, t, v, lane, count, sum, mm, gf, X);
     }
-    __syncwarp();
-    if (lane < qn) fast_exec<A, SM, MM, XS>(f_dsm[qb + lane], ((double *)&f_dsm[qb + QCAP])[lane], count, sum, mm, gf, X);
-
     unsigned long long in_w = n_in, out_w = rows - n_in;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {

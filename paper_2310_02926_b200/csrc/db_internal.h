@@ -152,6 +152,7 @@ cudaError_t launch_finalize(const Geom &g, const Accum &acc, Meta *meta_dev, int
                             int variant, cudaStream_t s);
 // bytes of shared memory per window bin
 int window_bytes_per_bin(const Accum &acc);
+int fast_window_bytes_per_bin(const Accum &acc);  // k_bin_fast's window (bin_fast.cu)
 
 
 // partition route (bin_part.cu): rows grouped by tile of Wt bins, then
