@@ -308,8 +308,14 @@ __global__ void __launch_bounds__(FAST_THREADS, 1)
     }
     c.fx = XS ? fx_param_exact(s_exp) : fx_param(HS ? s_exp : 0u);
     c.mm = acc.mm;
+    // rows: pairs [0, S) statically strided over the threads, then pairs [S,
+    // npairs) claimed by warps in blocks of 32 x TAIL_Q pairs from a counter
+    // (acc.window[7], zeroed by k_prep): equal static shares left the CTAs'
+    // end times 30-50 us apart (DATABIN_TRACE), idling SMs at the end
+    const uint32_t k1 = npairs / nthr - (npairs / nthr) / 8;
+    const uint32_t S = k1 * nthr;
     double2 bx[D], bv = make_double2(0.0, 0.0);
-    if (p0 < npairs) {
+    if (p0 < S) {
 #pragma unroll
         for (int d = 0; d < D; ++d) bx[d] = __ldcs(cx[d] + p0);
         if (A == 1) bv = __ldcs(cv + p0);
@@ -332,12 +338,12 @@ __global__ void __launch_bounds__(FAST_THREADS, 1)
     trace(1);
     uint32_t n_in = 0, rows = 0;
     {
-        for (uint32_t pb = p0 - lane; pb < npairs; pb += nthr) {  // warp-uniform trip count
+        for (uint32_t pb = p0 - lane; pb < S; pb += nthr) {  // warp-uniform trip count
             const uint32_t pc = pb + lane;
-            const bool valid = pc < npairs;
+            const bool valid = pc < S;
             const uint32_t pn = pc + nthr;
             double2 nx[D], nv = make_double2(0.0, 0.0);
-            if (pn < npairs) {
+            if (pn < S) {
 #pragma unroll
                 for (int d = 0; d < D; ++d) nx[d] = __ldcs(cx[d] + pn);
                 if (A == 1) nv = __ldcs(cv + pn);
@@ -368,6 +374,43 @@ __global__ void __launch_bounds__(FAST_THREADS, 1)
             bv = nv;
         }
     }
+    {  // the tail: blocks of 32 x TAIL_Q consecutive pairs per claim (coalesced)
+        constexpr uint32_t TAIL_Q = 16;
+        uint32_t *ctr = (uint32_t *)acc.window + 7;
+        for (;;) {
+            uint32_t base = 0;
+            if (lane == 0) base = atomicAdd(ctr, 32u * TAIL_Q);
+            base = __shfl_sync(0xffffffffu, base, 0) + S;
+            if (base >= npairs) break;
+            uint32_t pc = base + lane;
+            if (pc < npairs) {
+#pragma unroll
+                for (int d = 0; d < D; ++d) bx[d] = __ldcs(cx[d] + pc);
+                if (A == 1) bv = __ldcs(cv + pc);
+            }
+            for (uint32_t i = 0; i < TAIL_Q; ++i, pc += 32) {
+                const bool valid = pc < npairs;
+                const uint32_t pn = pc + 32;
+                double2 nx[D], nv = make_double2(0.0, 0.0);
+                if (i + 1 < TAIL_Q && pn < npairs) {
+#pragma unroll
+                    for (int d = 0; d < D; ++d) nx[d] = __ldcs(cx[d] + pn);
+                    if (A == 1) nv = __ldcs(cv + pn);
+                }
+                double x[D];
+#pragma unroll
+                for (int d = 0; d < D; ++d) x[d] = bx[d].x;
+                lean_row<D, A, SM, MM, XS>(c, x, bv.x, valid, n_in, count, sum, X);
+#pragma unroll
+                for (int d = 0; d < D; ++d) x[d] = bx[d].y;
+                lean_row<D, A, SM, MM, XS>(c, x, bv.y, valid, n_in, count, sum, X);
+                rows += valid ? 2u : 0u;
+#pragma unroll
+                for (int d = 0; d < D; ++d) bx[d] = nx[d];
+                bv = nv;
+            }
+        }
+    }
     // the unpaired head row (lane 0) and tail row (lane 1) of the whole input, on warp 0 of CTA 0
     if (blockIdx.x == 0 && threadIdx.x < 32) {
         const int64_t r = lane == 0 ? (head ? 0 : -1)
@@ -392,7 +435,9 @@ __global__ void __launch_bounds__(FAST_THREADS, 1)
     __syncthreads();
     trace(2);
 
-    // flush the window into the global accumulator (L2 reductions)
+    // flush the window into the global accumulator (L2 reductions; with the
+    // balanced tail all CTAs flush at once: ~25 us, vs ~10 us when their end
+    // times were spread.  Rotating each CTA's flush order measured slower.)
     for (uint32_t l = threadIdx.x; l < W; l += FAST_THREADS) {
         const unsigned long long cnt = f_dsm[c.o_cnt + l];
         if (cnt == 0) continue;

@@ -162,6 +162,7 @@ __global__ void __launch_bounds__(PREP_THREADS) k_prep(Geom g, Inputs in, Accum 
     const ulonglong2 ident = make_ulonglong2(~0ull, ~0ull);
     for (int64_t i = t0; i < (int64_t)(nb * acc.nmm); i += stride) ((ulonglong2 *)acc.mm)[i] = ident;
     if (t0 < 2 * g.ndim) acc.bounds[t0] = ~0ull;
+    if (t0 == 0) acc.window[7] = 0;  // k_bin_fast's tail work counter
     if (acc.xs) {  // exact sums: clear the digits the slot's previous execute touched (the
                    // range itself is reset by a stream-ordered memset after this kernel)
         for (int s = 0; s < acc.nsum; ++s) {
