@@ -402,8 +402,14 @@ def main():
             kname = f"k_bin_fast<{D},1,1,1>" if len(w.attrs) == 1 else f"k_bin_fast<{D},{len(w.attrs)},..>"
         else:
             kname = f"k_bin<{D},..>"
-        combine = ("fused NVLink peer-memory combine + finalize (k_combine_peer)" if var & 32
-                   else "NCCL allreduce of bin arrays + k_finalize") if world > 1 else "none (1 rank)"
+        if world == 1:
+            combine = "none (1 rank)"
+        elif var & 64:
+            combine = "NVLS in-switch combine + finalize (k_combine_nvls: multimem.ld_reduce / multimem.st)"
+        elif var & 32:
+            combine = "fused NVLink peer-memory combine + finalize (k_combine_peer)"
+        else:
+            combine = "NCCL allreduce of bin arrays + k_finalize"
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": args.scaling,

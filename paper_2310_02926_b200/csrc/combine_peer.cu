@@ -39,6 +39,12 @@ __global__ void __launch_bounds__(COMB_THREADS) k_combine_peer(Geom g, PeerSet p
     combine_peer_body<EXACT>(g, ps, rank, nranks, epoch, meta, variant, bulk != 0);
 }
 
+template <bool EXACT>
+__global__ void __launch_bounds__(COMB_THREADS) k_combine_nvls(Geom g, PeerSet ps, int rank, int nranks,
+                                                               unsigned long long epoch, Meta *meta, int variant) {
+    combine_nvls_body<EXACT>(g, ps, rank, nranks, epoch, meta, variant);
+}
+
 // One-device rank group (bin_execute_group): rank blockIdx.y runs the same
 // body over its own peer set; the group's ranks all live in this launch.
 template <bool EXACT>
@@ -56,6 +62,16 @@ cudaError_t launch_combine_peer(const Geom &g, const PeerSet &ps, int rank, int 
     const uint64_t B = ps.me.nbins;
     const uint64_t slice = (B + nranks - 1) / nranks;
     (void)deterministic;
+    if (ps.mc_count) {  // NVLS: in-switch reduction, one thread per bin of the slice
+        uint64_t blocks = (slice / 2 + COMB_THREADS - 1) / COMB_THREADS;  // a thread per bin pair
+        if (blocks > (uint64_t)sms * 8) blocks = (uint64_t)sms * 8;
+        if (blocks < 1) blocks = 1;
+        if (ps.me.xs)
+            k_combine_nvls<true><<<(unsigned)blocks, COMB_THREADS, 0, s>>>(g, ps, rank, nranks, epoch, meta, variant | 64);
+        else
+            k_combine_nvls<false><<<(unsigned)blocks, COMB_THREADS, 0, s>>>(g, ps, rank, nranks, epoch, meta, variant | 64);
+        return cudaGetLastError();
+    }
     static const bool no_bulk = getenv("DATABIN_COMBINE_BULK") && getenv("DATABIN_COMBINE_BULK")[0] == '0';
     const bool bulk = !no_bulk && !ps.me.xs && ps.me.nsum <= 1 && ps.me.nmm <= 1 &&
                       (nranks == 2 || nranks == 4 || nranks == 8);

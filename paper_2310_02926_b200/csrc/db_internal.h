@@ -8,6 +8,8 @@
 #include <string>
 #include <vector>
 
+#include <nccl.h>
+
 #include "../../include/databin.h"
 
 namespace db {
@@ -193,9 +195,30 @@ struct PeerSet {
     unsigned long long *flags[PEER_MAX];  // every rank's barrier words [A: 0..63][B: 64..127]
     unsigned *ctas_done;                  // this rank's last-CTA counter
     unsigned *ctas_failed;                // nonzero: a CTA of this rank timed out at barrier A
+    // NVLS: multicast addresses of this slot's arrays (the same offsets on every
+    // rank); mc_count == nullptr when the handle has no NVLS region
+    unsigned long long *mc_count;
+    double *mc_sum;
+    unsigned long long *mc_mm;
+    double *mc_omin, *mc_omax, *mc_oavg;
+    long long *mc_xs;
+    int32_t *mc_xrange;
 };
 cudaError_t launch_combine_peer(const Geom &g, const PeerSet &ps, int rank, int nranks, unsigned long long epoch,
                                 Meta *meta, int variant, int deterministic, int sms, cudaStream_t s);
+
+// NVLS multicast memory (nvls.cpp): unicast + multicast mappings of one region
+struct NvlsRegion {
+    void *uc = nullptr, *mc = nullptr;
+    size_t size = 0;
+    unsigned long long mem = 0, mch = 0;  // CUmemGenericAllocationHandle
+    int device = -1;
+    bool bound = false;
+};
+bool nvls_available(int device);
+bool nvls_setup(size_t bytes, int rank, int nranks, int device, ncclComm_t comm, cudaStream_t s,
+                const void *nccl_id128, NvlsRegion *out);
+void nvls_free(NvlsRegion &r);
 // a rank group on one device: the same combine body for all ranks in one launch
 // (blockIdx.y = rank); every CTA co-resides (<= sms CTAs in total)
 struct GroupRank {

@@ -22,6 +22,7 @@ enum { EV_STAGE = 0, EV_INIT0, EV_INIT1, EV_BOUNDS1, EV_WINDOW1, EV_BIN1, EV_COM
 struct Slot {
     Accum acc{};
     unsigned char *base = nullptr;  // the slot's single device allocation (IPC-exported in peer mode)
+    bool external = false;          // base lies in the handle's NVLS region (not cudaMalloc'ed)
     PeerSet peers{};
     Meta *meta_h = nullptr, *meta_d = nullptr;
     cudaEvent_t done = nullptr, released = nullptr, zeroed = nullptr;
@@ -104,6 +105,7 @@ struct bin_handle {
     unsigned char *part_base = nullptr;  // partition-route scratch (grown on demand)
     size_t part_bytes = 0;
     bin_group *group = nullptr;  // member of a one-device rank group (bin_init_group)
+    NvlsRegion nvls;             // multicast-bound memory holding both slots (NVLS combine)
     bool finalized = false;
 };
 
@@ -174,7 +176,10 @@ static int nccl_error(ncclResult_t r, const char *what) {
 
 static void free_slot(bin_handle *h, Slot &s) {
     DeviceGuard g(h->device);
-    if (s.acc.count) { cudaFree(s.acc.count); count_free((int64_t)s.dev_bytes); }
+    if (s.acc.count) {
+        if (!s.external) cudaFree(s.acc.count);
+        count_free((int64_t)s.dev_bytes);
+    }
     s.acc = Accum{};
     if (s.meta_h) { cudaFreeHost(s.meta_h); count_free((int64_t)sizeof(Meta)); }
     s.meta_h = s.meta_d = nullptr;
@@ -189,27 +194,41 @@ static void free_slot(bin_handle *h, Slot &s) {
     s.done = s.released = nullptr;
 }
 
-static int alloc_slot(bin_handle *h, Slot &s) {
+// One slot allocation's layout (all pieces 256-byte aligned).
+struct SlotLayout {
+    size_t count, sum, mm, bounds, window, fxexp, omin, omax, oavg, meta, xrange, xs, total;
+};
+static SlotLayout slot_layout(const bin_handle *h) {
     const uint64_t B = h->nbins;
-    // one device allocation, carved (all pieces 16-byte aligned)
     auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
-    size_t o_count = 0;
-    size_t o_sum = o_count + al((B + 2) * 8);
-    size_t o_mm = o_sum + al(B * 8 * h->nsum);
-    size_t o_bounds = o_mm + al(B * 16 * h->nmm);
-    size_t o_window = o_bounds + al(6 * 8);
-    size_t o_fxexp = o_window + al(8 * 4);
-    size_t o_omin = o_fxexp + al(16 * 4);
-    size_t o_omax = o_omin + al(B * 8 * h->nmm);
-    size_t o_oavg = o_omax + al(B * 8 * h->nmm);
-    size_t o_meta = o_oavg + al(B * 8 * h->nsum);
+    SlotLayout L;
+    L.count = 0;
+    L.sum = L.count + al((B + 2) * 8);
+    L.mm = L.sum + al(B * 8 * h->nsum);
+    L.bounds = L.mm + al(B * 16 * h->nmm);
+    L.window = L.bounds + al(6 * 8);
+    L.fxexp = L.window + al(8 * 4);
+    L.omin = L.fxexp + al(16 * 4);
+    L.omax = L.omin + al(B * 8 * h->nmm);
+    L.oavg = L.omax + al(B * 8 * h->nmm);
+    L.meta = L.oavg + al(B * 8 * h->nsum);
     const bool exact = h->spec.sum_mode == BIN_SUM_EXACT && h->nsum > 0;
-    size_t o_xrange = o_meta + al(sizeof(Meta));
-    size_t o_xs = o_xrange + al(2 * BIN_MAX_ATTR * 4);
-    size_t total = exact ? o_xs + al(B * 8 * XD_DIGITS * h->nsum) : o_xrange;
-    unsigned char *base = nullptr;
-    cudaError_t e = cudaMalloc(&base, total);
+    L.xrange = L.meta + al(sizeof(Meta));
+    L.xs = L.xrange + al(2 * BIN_MAX_ATTR * 4);
+    L.total = exact ? L.xs + al(B * 8 * XD_DIGITS * h->nsum) : L.xrange;
+    return L;
+}
+
+// ext: carve the slot from this memory (the NVLS region), else cudaMalloc it.
+static int alloc_slot(bin_handle *h, Slot &s, unsigned char *ext = nullptr) {
+    const uint64_t B = h->nbins;
+    const SlotLayout L = slot_layout(h);
+    const bool exact = h->spec.sum_mode == BIN_SUM_EXACT && h->nsum > 0;
+    const size_t total = L.total;
+    unsigned char *base = ext;
+    cudaError_t e = ext ? cudaSuccess : cudaMalloc(&base, total);
     s.base = base;
+    s.external = ext != nullptr;
     if (e != cudaSuccess) {
         cudaGetLastError();
         return set_error(BIN_ENOMEM, "bin_init: %zu bytes of bin arrays on device %d", total, h->device);
@@ -217,18 +236,18 @@ static int alloc_slot(bin_handle *h, Slot &s) {
     count_alloc((int64_t)total);
     s.dev_bytes = total;
     if ((e = cudaMemset(base, 0, total)) != cudaSuccess) return cuda_error(e, "bin_init memset");
-    s.acc.count = (unsigned long long *)(base + o_count);
-    s.acc.sum = (double *)(base + o_sum);
-    s.acc.mm = (unsigned long long *)(base + o_mm);
-    s.acc.bounds = (unsigned long long *)(base + o_bounds);
-    s.acc.window = (int32_t *)(base + o_window);
-    s.acc.fxexp = (uint32_t *)(base + o_fxexp);
-    s.acc.omin = (double *)(base + o_omin);
-    s.acc.omax = (double *)(base + o_omax);
-    s.acc.oavg = (double *)(base + o_oavg);
+    s.acc.count = (unsigned long long *)(base + L.count);
+    s.acc.sum = (double *)(base + L.sum);
+    s.acc.mm = (unsigned long long *)(base + L.mm);
+    s.acc.bounds = (unsigned long long *)(base + L.bounds);
+    s.acc.window = (int32_t *)(base + L.window);
+    s.acc.fxexp = (uint32_t *)(base + L.fxexp);
+    s.acc.omin = (double *)(base + L.omin);
+    s.acc.omax = (double *)(base + L.omax);
+    s.acc.oavg = (double *)(base + L.oavg);
     if (exact) {
-        s.acc.xrange = (int32_t *)(base + o_xrange);
-        s.acc.xs = (long long *)(base + o_xs);
+        s.acc.xrange = (int32_t *)(base + L.xrange);
+        s.acc.xs = (long long *)(base + L.xs);
         if ((e = cudaMemset(s.acc.xrange, 0x7f, 2 * BIN_MAX_ATTR * 4)) != cudaSuccess)
             return cuda_error(e, "bin_init memset(xrange)");
     }
@@ -243,7 +262,7 @@ static int alloc_slot(bin_handle *h, Slot &s) {
     DB_CUDA(cudaHostAlloc((void **)&s.meta_h, sizeof(Meta), cudaHostAllocPortable));
     count_alloc((int64_t)sizeof(Meta));
     memset(s.meta_h, 0, sizeof(Meta));
-    s.meta_d = (Meta *)(base + o_meta);
+    s.meta_d = (Meta *)(base + L.meta);
     DB_CUDA(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
     DB_CUDA(cudaEventCreateWithFlags(&s.released, cudaEventDisableTiming));
     DB_CUDA(cudaEventCreateWithFlags(&s.zeroed, cudaEventDisableTiming));
@@ -346,7 +365,8 @@ static bool setup_peer(bin_handle *h) {
         cudaMemset(h->flags, 0, 128 * sizeof(unsigned long long)) != cudaSuccess ||
         cudaMalloc(&h->ctas_done, 64) != cudaSuccess || cudaMemset(h->ctas_done, 0, 64) != cudaSuccess)
         mine.ok = 0;
-    for (int k = 0; k < 2 && mine.ok; ++k)
+    const bool nvls = h->nvls.mc != nullptr;  // slots in multicast memory: no unicast peer mappings needed
+    for (int k = 0; k < 2 && mine.ok && !nvls; ++k)
         if (cudaIpcGetMemHandle(&mine.slot[k], h->slot[k].base) != cudaSuccess) mine.ok = 0;
     if (mine.ok && cudaIpcGetMemHandle(&mine.flags, h->flags) != cudaSuccess) mine.ok = 0;
     cudaGetLastError();
@@ -380,7 +400,7 @@ static bool setup_peer(bin_handle *h) {
             continue;
         }
         void *ptr = nullptr;
-        for (int k = 0; k < 2 && good; ++k) {
+        for (int k = 0; k < 2 && good && !nvls; ++k) {
             if (cudaIpcOpenMemHandle(&ptr, rec[p].slot[k], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) good = false;
             else h->opened.push_back(ptr), slot_base[p][k] = (unsigned char *)ptr;
         }
@@ -410,6 +430,21 @@ static bool setup_peer(bin_handle *h) {
         auto rel = [&](const void *local, int p) {
             return slot_base[p][k] + ((const unsigned char *)local - S.base);
         };
+        if (nvls) {  // the combine reads and writes every rank through the multicast mapping
+            auto mc = [&](const void *local) {
+                return (unsigned char *)h->nvls.mc + ((const unsigned char *)local - (const unsigned char *)h->nvls.uc);
+            };
+            ps.mc_count = (unsigned long long *)mc(S.acc.count);
+            ps.mc_sum = (double *)mc(S.acc.sum);
+            ps.mc_mm = (unsigned long long *)mc(S.acc.mm);
+            ps.mc_omin = (double *)mc(S.acc.omin);
+            ps.mc_omax = (double *)mc(S.acc.omax);
+            ps.mc_oavg = (double *)mc(S.acc.oavg);
+            ps.mc_xs = S.acc.xs ? (long long *)mc(S.acc.xs) : nullptr;
+            ps.mc_xrange = S.acc.xrange ? (int32_t *)mc(S.acc.xrange) : nullptr;
+            for (int p = 0; p < R; ++p) ps.flags[p] = flags[p];
+            continue;
+        }
         for (int p = 0; p < R; ++p) {
             ps.count[p] = (unsigned long long *)rel(S.acc.count, p);
             ps.sum[p] = (double *)rel(S.acc.sum, p);
@@ -507,8 +542,31 @@ int bin_init(const bin_spec_t *spec, const bin_placement_t *place, const bin_com
     h->wcap = (h->lc.smem_optin - static_smem - qbytes) / bpb;
     h->smem_bytes = (int)((uint64_t)h->wcap >= B ? B * bpb : (uint64_t)h->wcap * bpb);
     h->smem_bytes = ((h->smem_bytes + 15) & ~15) + qbytes;
-    for (auto &s : h->slot)
-        if ((rc = alloc_slot(h, s))) return fail(rc);
+    if (nranks > 1) {  // the communicator first: the NVLS region is a collective allocation
+        ncclUniqueId id;
+        memcpy(&id, comm->nccl_unique_id, sizeof id);
+        ncclResult_t r = ncclCommInitRank(&h->comm, nranks, id, rank);
+        if (r != ncclSuccess) {
+            h->comm = nullptr;
+            return fail(nccl_error(r, "ncclCommInitRank"));
+        }
+    }
+    // NVLS combine (DATABIN_COMBINE=nvls, every GPU supporting multicast): both
+    // slots in one multicast-bound region, reduced in the switch.  Measured
+    // slower than the IPC peer combine's TMA bulk copies at 2 and 4 ranks on
+    // C3 (slice 52-62 us vs 20-40 us: 8-byte multimem requests are rate-bound),
+    // so the peer combine stays the default (DATABIN_COMBINE=nccl: NCCL).
+    // Deterministic sums need the rank-ordered fold, which the switch does not keep.
+    const size_t slot_sz = (slot_layout(h).total + 4095) & ~(size_t)4095;
+    {
+        const char *env = getenv("DATABIN_COMBINE");
+        const bool want = nranks > 1 && nranks <= PEER_MAX && !spec->deterministic && env && strcmp(env, "nvls") == 0;
+        if (want && !nvls_setup(2 * slot_sz, rank, nranks, dev, h->comm, h->side, comm->nccl_unique_id, &h->nvls))
+            h->nvls = NvlsRegion{};
+    }
+    for (int k = 0; k < 2; ++k)
+        if ((rc = alloc_slot(h, h->slot[k], h->nvls.uc ? (unsigned char *)h->nvls.uc + k * slot_sz : nullptr)))
+            return fail(rc);
     if ((ce = cudaMalloc(&h->wcache, (size_t)h->lc.sms * 8 * sizeof(int32_t))) != cudaSuccess)
         return fail(cuda_error(ce, "cudaMalloc(window cache)"));
     count_alloc((int64_t)h->lc.sms * 32);
@@ -525,16 +583,7 @@ int bin_init(const bin_spec_t *spec, const bin_placement_t *place, const bin_com
         h->gather = (double *)dev_alloc(h->gather_bytes, dev, nullptr, false);
         if (!h->gather) return fail(set_error(BIN_ENOMEM, "deterministic gather buffer"));
     }
-    if (nranks > 1) {
-        ncclUniqueId id;
-        memcpy(&id, comm->nccl_unique_id, sizeof id);
-        ncclResult_t r = ncclCommInitRank(&h->comm, nranks, id, rank);
-        if (r != ncclSuccess) {
-            h->comm = nullptr;
-            return fail(nccl_error(r, "ncclCommInitRank"));
-        }
-        h->peer = setup_peer(h);
-    }
+    if (nranks > 1) h->peer = setup_peer(h);
     *out = h;
     return BIN_OK;
 }
@@ -899,7 +948,7 @@ static int execute_impl(bin_handle *h, bin_array_t *const *axes, int32_t naxes, 
                                      h->spec.deterministic, h->lc.sms, s)) != cudaSuccess)
             return cuda_error(e, "peer combine kernel");
         S.launches++;
-        S.variant = variant | 32;
+        S.variant = variant | 32 | (S.peers.mc_count ? 64 : 0);
         if ((rc = rec(EV_FINAL1, true))) return rc;
     } else {
     // ---- a6: cross-rank combine over NVLink (one NCCL group)
@@ -1267,6 +1316,7 @@ int bin_finalize(bin_handle_t *h) {
         }
         group_drop(h);
         for (auto &S : h->slot) free_slot(h, S);
+        nvls_free(h->nvls);
         for (auto &row : h->stage)
             for (auto &st : row)
                 if (st.p) {

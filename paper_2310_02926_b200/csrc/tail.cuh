@@ -448,4 +448,212 @@ __device__ __forceinline__ void combine_peer_body(const Geom &g, const PeerSet &
     }
 }
 
+// ---------------------------------------------------------------- NVLS combine [a6 + a7]
+// The same barriers and slice ownership as combine_peer_body, but the slice
+// is reduced IN THE SWITCH: multimem.ld_reduce on the multicast address reads
+// every rank's copy of a word and returns their sum / min (count Sum u64, sum
+// Sum f64 -- order unspecified, reading R8 --, min/max Min u64, exact-sum digits
+// Sum u64), and multimem.st writes the finalized values into every rank's
+// arrays with one store.  Per rank and bin of its slice that is 8 B x words
+// read and written once over NVLink instead of nranks times.
+__device__ __forceinline__ unsigned long long mc_add_u64(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.u64 %0, [%1];" : "=l"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ double mc_add_f64(const double *p) {
+    double v;
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ unsigned long long mc_min_u64(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.min.u64 %0, [%1];" : "=l"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ int mc_min_s32(const int *p) {
+    int v;
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.min.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void mc_st_u64(unsigned long long *p, unsigned long long v) {
+    asm volatile("multimem.st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void mc_st_f64(double *p, double v) {
+    asm volatile("multimem.st.relaxed.sys.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+// 16 bytes (two 64-bit words, bit patterns kept) to every rank in one request
+__device__ __forceinline__ void mc_st_2x64(void *p, unsigned long long a, unsigned long long b) {
+    asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p),
+                 "f"(__uint_as_float((unsigned)a)), "f"(__uint_as_float((unsigned)(a >> 32))),
+                 "f"(__uint_as_float((unsigned)b)), "f"(__uint_as_float((unsigned)(b >> 32)))
+                 : "memory");
+}
+
+template <bool EXACT>
+__device__ __forceinline__ void combine_nvls_body(const Geom &g, const PeerSet &ps, int rank, int nranks,
+                                                  unsigned long long epoch, Meta *meta, int variant) {
+    __shared__ bool ok_s, last_s;
+    const Accum &me = ps.me;
+    const uint64_t B = me.nbins;
+    // ---- barrier A: all partial accumulators complete
+    if (threadIdx.x == 0) {
+        if (blockIdx.x == 0) {
+            meta->trace[0] = globaltimer();
+            __threadfence_system();
+            for (int p = 0; p < nranks; ++p) st_release_sys(ps.flags[p] + rank, epoch);
+        }
+        ok_s = wait_all(ps.flags[rank], nranks, epoch);
+        if (!ok_s) atomicOr(ps.ctas_failed, 1u);
+        if (blockIdx.x == 0) {
+            meta->trace[1] = globaltimer();
+            if (ok_s) {  // summed over the ranks now (after barrier B a peer may re-zero them)
+                meta->n_in = mc_add_u64(ps.mc_count + B);
+                meta->n_out = mc_add_u64(ps.mc_count + B + 1);
+            }
+        }
+    }
+    __syncthreads();
+    const bool ok = ok_s;
+    const uint64_t s0 = (B * (uint64_t)rank) / nranks, s1 = (B * (uint64_t)(rank + 1)) / nranks;
+    const int nsum = me.nsum, nmm = me.nmm;
+    const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+    const double pinf = __longlong_as_double(0x7ff0000000000000ll);
+    const double ninf = __longlong_as_double((long long)0xfff0000000000000ull);
+    __shared__ int s_klo[BIN_MAX_ATTR], s_khi[BIN_MAX_ATTR];
+    if (EXACT && threadIdx.x < nsum) {  // the union of the ranks' touched digit ranges
+        const int lo = mc_min_s32(ps.mc_xrange + 2 * threadIdx.x), nhi = mc_min_s32(ps.mc_xrange + 2 * threadIdx.x + 1);
+        s_klo[threadIdx.x] = lo == XR_EMPTY ? 1 : lo;
+        s_khi[threadIdx.x] = lo == XR_EMPTY ? 0 : -nhi;
+    }
+    if (EXACT) __syncthreads();
+    // bins in pairs (16-byte multimem stores: the switch's small-request rate,
+    // not link bandwidth, bounds this loop); an unpaired edge bin on each side
+    const uint64_t e0 = (s0 + 1) & ~1ull, e1 = s1 & ~1ull;
+    auto one_pair = [&](uint64_t b, bool two) {
+        const int H = two ? 2 : 1;
+        if (!EXACT && nsum <= 1 && nmm <= 1) {  // common case: every load in flight before any store
+            unsigned long long cnt[2] = {0ull, 0ull}, mn[2] = {~0ull, ~0ull}, nx[2] = {~0ull, ~0ull};
+            double sm[2] = {0.0, 0.0};
+            for (int h = 0; h < H; ++h) {
+                cnt[h] = mc_add_u64(ps.mc_count + b + h);
+                if (nsum) sm[h] = mc_add_f64(ps.mc_sum + b + h);
+                if (nmm) {
+                    mn[h] = mc_min_u64(ps.mc_mm + 2 * (b + h));
+                    nx[h] = mc_min_u64(ps.mc_mm + 2 * (b + h) + 1);
+                }
+            }
+            double av[2], lo[2], hi[2];
+            for (int h = 0; h < 2; ++h) {
+                av[h] = cnt[h] ? __ddiv_rn(sm[h], (double)cnt[h]) : qnan;
+                lo[h] = cnt[h] ? dec_total(mn[h]) : pinf;
+                hi[h] = cnt[h] ? dec_total(~nx[h]) : ninf;
+            }
+            if (two) {
+                mc_st_2x64(ps.mc_count + b, cnt[0], cnt[1]);
+                if (nsum) {
+                    mc_st_2x64(ps.mc_sum + b, __double_as_longlong(sm[0]), __double_as_longlong(sm[1]));
+                    mc_st_2x64(ps.mc_oavg + b, __double_as_longlong(av[0]), __double_as_longlong(av[1]));
+                }
+                if (nmm) {
+                    mc_st_2x64(ps.mc_omin + b, __double_as_longlong(lo[0]), __double_as_longlong(lo[1]));
+                    mc_st_2x64(ps.mc_omax + b, __double_as_longlong(hi[0]), __double_as_longlong(hi[1]));
+                }
+            } else {
+                mc_st_u64(ps.mc_count + b, cnt[0]);
+                if (nsum) mc_st_f64(ps.mc_sum + b, sm[0]), mc_st_f64(ps.mc_oavg + b, av[0]);
+                if (nmm) mc_st_f64(ps.mc_omin + b, lo[0]), mc_st_f64(ps.mc_omax + b, hi[0]);
+            }
+            return;
+        }
+        unsigned long long cnt[2];
+        cnt[0] = mc_add_u64(ps.mc_count + b);
+        cnt[1] = two ? mc_add_u64(ps.mc_count + b + 1) : 0ull;
+        if (two) mc_st_2x64(ps.mc_count + b, cnt[0], cnt[1]);
+        else mc_st_u64(ps.mc_count + b, cnt[0]);
+        for (int s = 0; s < nsum; ++s) {
+            double sm[2], av[2];
+            for (int h = 0; h < H; ++h) {
+                if constexpr (EXACT) {  // digits add as integers in the switch, then one rounding
+                    long long d[XD];
+                    const int klo = s_klo[s], khi = s_khi[s];
+                    for (int k = klo; k <= khi; ++k)
+                        d[k - klo] = (long long)mc_add_u64((const unsigned long long *)ps.mc_xs +
+                                                           ((uint64_t)s * XD + k) * B + b + h);
+                    sm[h] = cnt[h] ? xsum_round_digits(d, klo, khi) : 0.0;
+                } else {
+                    sm[h] = mc_add_f64(ps.mc_sum + (uint64_t)s * B + b + h);
+                }
+                av[h] = cnt[h] ? __ddiv_rn(sm[h], (double)cnt[h]) : qnan;
+            }
+            double *ds = ps.mc_sum + (uint64_t)s * B + b, *da = ps.mc_oavg + (uint64_t)s * B + b;
+            if (two) {
+                mc_st_2x64(ds, __double_as_longlong(sm[0]), __double_as_longlong(sm[1]));
+                mc_st_2x64(da, __double_as_longlong(av[0]), __double_as_longlong(av[1]));
+            } else {
+                mc_st_f64(ds, sm[0]);
+                mc_st_f64(da, av[0]);
+            }
+        }
+        for (int s = 0; s < nmm; ++s) {
+            double mn[2], mx[2];
+            for (int h = 0; h < (two ? 2 : 1); ++h) {
+                const uint64_t w = 2 * ((uint64_t)s * B + b + h);
+                const unsigned long long m = mc_min_u64(ps.mc_mm + w), nx = mc_min_u64(ps.mc_mm + w + 1);
+                mn[h] = cnt[h] ? dec_total(m) : pinf;
+                mx[h] = cnt[h] ? dec_total(~nx) : ninf;
+            }
+            double *dn = ps.mc_omin + (uint64_t)s * B + b, *dx = ps.mc_omax + (uint64_t)s * B + b;
+            if (two) {
+                mc_st_2x64(dn, __double_as_longlong(mn[0]), __double_as_longlong(mn[1]));
+                mc_st_2x64(dx, __double_as_longlong(mx[0]), __double_as_longlong(mx[1]));
+            } else {
+                mc_st_f64(dn, mn[0]);
+                mc_st_f64(dx, mx[0]);
+            }
+        }
+    };
+    if (ok && e0 < e1) {
+        for (uint64_t j = e0 / 2 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < e1 / 2;
+             j += (uint64_t)gridDim.x * blockDim.x)
+            one_pair(2 * j, true);
+    }
+    if (ok && blockIdx.x == 0 && threadIdx.x < 2) {  // edge bins
+        if (e0 < e1) {
+            if (threadIdx.x == 0 && s0 < e0) one_pair(s0, false);
+            if (threadIdx.x == 1 && e1 < s1) one_pair(e1, false);
+        } else if (threadIdx.x == 0) {
+            for (uint64_t b = s0; b < s1; ++b) one_pair(b, false);
+        }
+    }
+    // ---- barrier B: every slice written everywhere
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) last_s = atomicAdd(ps.ctas_done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last_s) return;
+    if (threadIdx.x == 0) {
+        meta->trace[2] = globaltimer();
+        *ps.ctas_done = 0u;
+        const bool failed = atomicExch(ps.ctas_failed, 0u) != 0u;
+        __threadfence_system();
+        const unsigned long long fb = epoch | (failed ? PEER_FAIL : 0ull);
+        for (int p = 0; p < nranks; ++p) st_release_sys(ps.flags[p] + 64 + rank, fb);
+        bool peer_failed = false;
+        const bool ok2 = !failed && wait_all(ps.flags[rank] + 64, nranks, epoch, &peer_failed) && !peer_failed;
+        const DGeom G = load_geom(g, me.bounds);
+        meta->status = !ok2 ? BIN_ENCCL : (G.ok ? 0 : BIN_EDEGENERATE);
+        meta->variant = variant;
+        for (int d = 0; d < 3; ++d) {
+            meta->lo[d] = G.lo[d];
+            meta->hi[d] = G.hi[d];
+            meta->window[d] = me.window[d];
+            meta->window[3 + d] = me.window[3 + d];
+        }
+        meta->done = 1;
+        meta->trace[3] = globaltimer();
+        for (int a = 0; a < BIN_MAX_ATTR; ++a) me.fxexp[a] = 0u;
+    }
+}
+
 }  // namespace db

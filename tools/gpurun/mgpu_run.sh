@@ -14,3 +14,7 @@ if [ "${AB_NCCL:-0}" = "1" ]; then
 DATABIN_COMBINE=nccl timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29514 bench.py --gpus $N --steps 100 --warmup 5 --no-cpu-baseline --no-e2e > gpurun_out/bench_n${N}_nccl.json 2>> gpurun_out/bench_n$N.err; echo bench_nccl=$?
 python tools/bench_lines.py gpurun_out/bench_n${N}_nccl.json
 fi
+if [ "${AB_PEER:-0}" = "1" ]; then
+DATABIN_COMBINE=peer timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29516 bench.py --gpus $N --steps 100 --warmup 5 --no-cpu-baseline --no-e2e > gpurun_out/bench_n${N}_peer.json 2>> gpurun_out/bench_n$N.err; echo bench_peer=$?
+python tools/bench_lines.py gpurun_out/bench_n${N}_peer.json
+fi
