@@ -33,6 +33,8 @@
 // per-row global atomics.  Row order inside a tile is not kept (atomic mode).
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
 
 #include "db_internal.h"
 #include "dev_common.cuh"
@@ -702,6 +704,41 @@ __global__ void __launch_bounds__(PART_THREADS, 1) k_part_reduce(Accum acc, Part
     if (XS) xr_publish(s_xr, acc.nsum, acc.xrange);  // (after the last tile's barrier)
 }
 
+
+// DATABIN_PART_TIMING=1 (diagnosis): CUDA events between the partition-route
+// kernels of every execute; averages printed at exit.
+namespace {
+struct PartTiming {
+    bool on = getenv("DATABIN_PART_TIMING") != nullptr;
+    cudaEvent_t ev[8] = {};
+    double ms[8] = {};
+    int n = 0, k = 0;
+    void mark(cudaStream_t s) {
+        if (!on) return;
+        if (!ev[k]) cudaEventCreate(&ev[k]);
+        cudaEventRecord(ev[k++], s);
+    }
+    void collect() {
+        if (!on || k < 2) return;
+        cudaEventSynchronize(ev[k - 1]);
+        for (int i = 1; i < k; ++i) {
+            float m = 0;
+            cudaEventElapsedTime(&m, ev[i - 1], ev[i]);
+            ms[i] += m;
+        }
+        ++n;
+        k = 0;
+    }
+    ~PartTiming() {
+        if (!on || !n) return;
+        fprintf(stderr, "[databin part timing] %d executes, ms per execute:", n);
+        for (int i = 1; i < 8; ++i) fprintf(stderr, " %.4f", ms[i] / n);
+        fprintf(stderr, "\n");
+    }
+};
+PartTiming g_pt;
+}  // namespace
+
 // ---------------------------------------------------------------- host side
 int part_bytes_per_bin(const Accum &acc) { return 4 + 12 * acc.nsum + 16 * acc.nmm; }
 
@@ -783,6 +820,7 @@ static cudaError_t launch_part_tail(const Inputs &in, const Accum &acc, const Pa
     const size_t sm0 = ((size_t)pa.C + 1 + 33) * 4;
     if ((e = cudaFuncSetAttribute(k_part_scan1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm0)) != cudaSuccess)
         return e;
+    g_pt.mark(s);
     k_part_scan1<<<pa.T1, 1024, sm0, s>>>(pa);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     const size_t sm1 = ((size_t)pa.T + 33) * 4;
@@ -794,7 +832,9 @@ static cudaError_t launch_part_tail(const Inputs &in, const Accum &acc, const Pa
     const size_t sm2 = scatter_smem(A, PPT);
     auto k2 = k_part_scatter<A, PPT, SC_THREADS>;
     if ((e = cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2)) != cudaSuccess) return e;
+    g_pt.mark(s);
     k2<<<pa.C, SC_THREADS, sm2, s>>>(in, pa);
+    g_pt.mark(s);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     *launches = 5;
     if (pa.G1 > 1) {
@@ -803,6 +843,7 @@ static cudaError_t launch_part_tail(const Inputs &in, const Accum &acc, const Pa
         if ((e = cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smr)) != cudaSuccess)
             return e;
         kr<<<pa.C, SC_THREADS, smr, s>>>(pa);
+        g_pt.mark(s);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
         *launches = 6;
     }
@@ -810,12 +851,15 @@ static cudaError_t launch_part_tail(const Inputs &in, const Accum &acc, const Pa
     auto k3 = acc.xs ? k_part_reduce<A, true> : k_part_reduce<A, false>;
     if ((e = cudaFuncSetAttribute(k3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm3)) != cudaSuccess) return e;
     k3<<<pa.C / 2, PART_THREADS, sm3, s>>>(acc, pa);  // one 1024-thread CTA per SM (C = 2 x SMs)
+    g_pt.mark(s);
+    g_pt.collect();
     return cudaGetLastError();
 }
 
 cudaError_t launch_partition(const Geom &g, const Inputs &in, const Accum &acc, const PartArgs &pa, cudaStream_t s,
                              int *launches) {
     cudaError_t e;
+    g_pt.mark(s);
     switch (g.ndim) {
     case 1: e = launch_keys_d<1>(g, in, acc, pa, s); break;
     case 2: e = launch_keys_d<2>(g, in, acc, pa, s); break;
