@@ -126,6 +126,9 @@ __device__ __forceinline__ void lean_row(const FastCtx<D> &c, const double (&x)[
     if (D >= 3) b += (uint32_t)(c.resm1[0] + 1) * (uint32_t)(c.resm1[D > 2 ? 1 : 0] + 1) * (uint32_t)k[D > 2 ? 2 : 0];
     const bool glob = ok && !inw;
     const uint32_t W = c.W;
+    DB_CHECK(!inw || l < W);
+#pragma unroll
+    for (int d = 0; d < D; ++d) DB_CHECK(!ok || (k[d] >= 0 && k[d] <= c.resm1[d]));
     ps_add(inw, c.sb + 4u * (c.o_cnt + l), 1u);
     bool sum_glob = glob;
     if (HS) {
@@ -223,6 +226,7 @@ __device__ __forceinline__ void fast_choose_window(const DGeom G, const WinPlan 
                 cell += (kd / P.cs[d]) * mul;
                 mul *= P.nc[d];
             }
+            DB_CHECK(!inside || (cell >= 0 && cell < WIN_CELLS));
             if (inside) atomicAdd(&f_dsm[cell], 1u);
         }
     }
@@ -449,6 +453,7 @@ __global__ void __launch_bounds__(FAST_THREADS, 1)
             b += kd * mul;
             mul *= (uint32_t)res[d];
         }
+        DB_CHECK(b < acc.nbins);
         atomicAdd(&count[b], cnt);
         if (HS) {
             const uint32_t w0 = c.o_fx + l;

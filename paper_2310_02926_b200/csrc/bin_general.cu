@@ -85,6 +85,9 @@ __device__ __forceinline__ void accumulate_row(const GenCtx &c, const FxParam (&
         l = l * c.w.we[d] + r;
     }
     const uint32_t W = c.w.W;
+    DB_CHECK(!inw || l < W);
+#pragma unroll
+    for (int d = 0; d < D; ++d) DB_CHECK(k[d] >= 0 && k[d] <= c.w.resm1[d]);
     if (inw) {
         atomicAdd(&g_dsm[c.o_cnt + l], 1u);
 #pragma unroll

@@ -122,6 +122,7 @@ __global__ void __launch_bounds__(NT, 2) k_part_keys(Geom g, Inputs in, Accum ac
     auto one = [&](const double (&x)[D]) -> uint32_t {
         const uint32_t b = part_key<D>(G, x);
         if (b != ~0u) {
+            DB_CHECK(b / Wt < T && b < acc.nbins);
             atomicAdd(&hist[b / Wt], 1u);
             ++n_in;
         }
@@ -352,6 +353,7 @@ __global__ void __launch_bounds__(NT, 2) k_part_scatter(Inputs in, PartArgs pa) 
         for (int r = 0; r < 2 * PPT; ++r) {
             if (key[r] == ~0u) continue;
             const uint32_t pos = boff[g[r]] + rk[r], li = (r >> 1) * NT + threadIdx.x;
+            DB_CHECK(g[r] < ng && pos < (uint32_t)R);
             st_key[pos] = key[r];
             st_g[pos] = (uint8_t)g[r];
 #pragma unroll
@@ -366,6 +368,7 @@ __global__ void __launch_bounds__(NT, 2) k_part_scatter(Inputs in, PartArgs pa) 
         for (uint32_t i = threadIdx.x; i < nst; i += NT) {
             const uint32_t gg = st_g[i];
             const uint64_t gp = (uint64_t)gbase[gg] + (i - boff[gg]);
+            DB_CHECK(gg < ng && gp < cap && gp >= pa.tstart[gg * pa.G1] && gp < pa.tstart[min(pa.T, (gg + 1) * pa.G1)]);
             __stcg(okey + gp, st_key[i]);
 #pragma unroll
             for (int j = 0; j < A; ++j)
@@ -490,6 +493,7 @@ __global__ void __launch_bounds__(NT, 2) k_part_refine(PartArgs pa) {
         for (int q = 0; q < RPT; ++q) {
             if (key[q] == ~0u) continue;
             const uint32_t pos = boff[g[q]] + rk[q], li = q * NT + threadIdx.x;
+            DB_CHECK(g[q] < ngt && pos < (uint32_t)R);
             st_key[pos] = key[q];
             st_g[pos] = (uint8_t)g[q];
 #pragma unroll
@@ -501,6 +505,7 @@ __global__ void __launch_bounds__(NT, 2) k_part_refine(PartArgs pa) {
         for (uint32_t i = threadIdx.x; i < nst; i += NT) {
             const uint32_t gg = st_g[i];
             const uint64_t gp = (uint64_t)gbase[gg] + (i - boff[gg]);
+            DB_CHECK(gp >= pa.tstart[tb + gg] && gp < pa.tstart[tb + gg + 1]);
             __stcg(pa.skey + gp, st_key[i]);
 #pragma unroll
             for (int j = 0; j < A; ++j)
@@ -634,6 +639,7 @@ __global__ void __launch_bounds__(PART_THREADS, 1) k_part_reduce(Accum acc, Part
             for (int u = 0; u < U; ++u) {
                 if (ck[u] == ~0u) continue;
                 const uint32_t l = ck[u] - bl;
+                DB_CHECK(l < W);
                 atomicAdd(&p_dsm[o_cnt + l], 1u);
 #pragma unroll
                 for (int j = 0; j < A; ++j) {

@@ -178,6 +178,7 @@ __global__ void __launch_bounds__(RS_THREADS, 3) k_rs_scatter(const uint32_t *ke
         if (i >= n) continue;
         const uint32_t d = (key[r] >> shift) & mask;
         const uint32_t idx = dstart[d] + wcnt[w][d] + lr[r];
+        DB_CHECK(idx < (uint32_t)RS_TILE);
         skey[idx] = key[r];
         spay[idx] = __ldcs(pay + i);
     }
@@ -186,6 +187,7 @@ __global__ void __launch_bounds__(RS_THREADS, 3) k_rs_scatter(const uint32_t *ke
     for (int64_t i = threadIdx.x; i < cnt; i += RS_THREADS) {  // contiguous runs per digit
         const uint32_t k = skey[i], d = (k >> shift) & mask;
         const uint64_t gp = (uint64_t)goff[d] + (uint64_t)(i - dstart[d]);
+        DB_CHECK(gp < (uint64_t)n);
         keys_out[gp] = k;
         pay_out[gp] = spay[i];
     }

@@ -8,6 +8,26 @@
 
 namespace db {
 
+// Checked build (-DDATABIN_CHECKED, tools/build_variants.py checked=DATABIN_CHECKED):
+// device-side bounds checks on every computed shared-memory window index,
+// global bin index and scatter position; a failing check prints its site and
+// traps, so the execute fails loudly at bin_wait.  (compute-sanitizer is not
+// available on the GPU pool: profiles/r02_compute_sanitizer_closed.txt.)
+#ifdef DATABIN_CHECKED
+#define DB_CHECK(c)                                                                             \
+    do {                                                                                        \
+        if (!(c)) {                                                                             \
+            printf("DB_CHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #c,  \
+                   (int)blockIdx.x, (int)threadIdx.x);                                         \
+            __trap();                                                                           \
+        }                                                                                       \
+    } while (0)
+#else
+#define DB_CHECK(c) \
+    do {            \
+    } while (0)
+#endif
+
 __device__ __forceinline__ unsigned long long enc_total(double x) {
     unsigned long long b = (unsigned long long)__double_as_longlong(x);
     unsigned long long m = (unsigned long long)((long long)b >> 63);

@@ -220,6 +220,7 @@ __global__ void __launch_bounds__(MULTI_THREADS) k_multi_bin(MultiArgs a) {
                 if (bo) atomicAdd(&s_out[k], (unsigned)__popc(bo));
             }
             if (!in) continue;
+            DB_CHECK(b < o.nbins);
             red_add_u64(&o.count[b], 1ull);
             const uint64_t B = o.nbins;
             // fire-and-forget L2 reductions only (an L2 load to filter the

@@ -1,8 +1,12 @@
-"""Small-input driver for compute-sanitizer (memcheck / racecheck / synccheck /
-initcheck): every kernel family of libdatabin once, on C1 and a few small
-random and route-forcing cases, each checked against the oracle so a run that
-the sanitizer slows down still proves it computed the right thing.
+"""Small-input driver for memory-safety runs: every kernel family of
+libdatabin once, on C1 and a few small random and route-forcing cases, each
+checked against the oracle.  Run it under compute-sanitizer where that is
+available, or (as on this GPU pool, where compute-sanitizer is closed) against
+the checked build, whose kernels bounds-check every computed window index,
+bin index and scatter position and trap on a failure:
 
+  python tools/build_variants.py checked=DATABIN_CHECKED
+  DATABIN_LIB=paper_2310_02926_b200/variants/checked.so python tools/sanitize.py
   compute-sanitizer --tool racecheck python tools/sanitize.py [--quick]
 
 Kernels covered: k_prep, k_bounds, k_probe, k_bin_fast (full-grid and hot
