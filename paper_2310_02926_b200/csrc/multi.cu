@@ -130,6 +130,9 @@ cudaError_t launch_multi_bounds(const MultiArgs &a, const LaunchCfg &lc, cudaStr
 // compiler cannot prove they are global and atomicAdd/atomicMin become generic
 // returning ATOMs (one L2 round trip each; measured 2x slower than k_bin's
 // global path).  Explicit fire-and-forget global reductions instead:
+#ifndef BIN_MULTI_MM_FILTER
+#define BIN_MULTI_MM_FILTER 1
+#endif
 __device__ __forceinline__ void red_add_u64(unsigned long long *p, unsigned long long v) {
     asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(__cvta_generic_to_global(p)), "l"(v) : "memory");
 }
@@ -223,20 +226,39 @@ __global__ void __launch_bounds__(MULTI_THREADS) k_multi_bin(MultiArgs a) {
             DB_CHECK(b < o.nbins);
             red_add_u64(&o.count[b], 1ull);
             const uint64_t B = o.nbins;
-            // fire-and-forget L2 reductions only (an L2 load to filter the
-            // min/max reductions, as k_bin_fast does for its rare global rows,
-            // serialises behind the preceding reductions: slower here)
-            for (int j = 0; j < o.nattr; ++j) {
-                const double v = sv[o.atc[j]][threadIdx.x];
-                if (o.sslot[j] >= 0) {
+            // attributes in chunks of 8: the chunk's min/max slot pairs are loaded
+            // from L2 first, then the count / sum reductions are fired while the
+            // loads are in flight, and a min or max reduction is sent only when
+            // the row improves the loaded value (slots only decrease, so a stale
+            // load can only let a reduction through, never skip a needed one):
+            // ~1 reduction per row and instance instead of 2 x attributes
+            // (BIN_MULTI_MM_FILTER=0: reduce every min/max unconditionally)
+            for (int j0 = 0; j0 < o.nattr; j0 += 8) {
+                ulonglong2 cur[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int j = j0 + u;
+                    cur[u] = make_ulonglong2(~0ull, ~0ull);
+                    if (BIN_MULTI_MM_FILTER && j < o.nattr && o.mslot[j] >= 0)
+                        cur[u] = __ldcg(o.mm + (uint64_t)o.mslot[j] * B + b);
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int j = j0 + u;
+                    if (j >= o.nattr || o.sslot[j] < 0) continue;
+                    const double v = sv[o.atc[j]][threadIdx.x];
                     if (o.xs) xsum_add_double(o.xs, B, o.sslot[j], b, v, s_xr[k]);
                     else red_add_f64(&o.sum[(uint64_t)o.sslot[j] * B + b], v);
                 }
-                if (o.mslot[j] >= 0) {
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int j = j0 + u;
+                    if (j >= o.nattr || o.mslot[j] < 0) continue;
+                    const double v = sv[o.atc[j]][threadIdx.x];
                     ulonglong2 *p = o.mm + (uint64_t)o.mslot[j] * B + b;
                     const unsigned long long e = enc_total(v);
-                    red_min_u64(&p->x, e);
-                    red_min_u64(&p->y, ~e);
+                    if (e < cur[u].x) red_min_u64(&p->x, e);
+                    if (~e < cur[u].y) red_min_u64(&p->y, ~e);
                 }
             }
         }
