@@ -149,7 +149,7 @@ cudaError_t launch_bin_general(const Geom &g, const Inputs &in, const Accum &acc
 cudaError_t launch_bin_fast(const Geom &g, const Inputs &in, const Accum &acc, const LaunchCfg &lc, int smem,
                             int wcap, int32_t *wcache, int reuse, unsigned long long *ktrace, cudaStream_t s);
 bool fast_eligible(const Inputs &in, const Accum &acc, int ndim);
-int fast_queue_bytes();
+int fast_queue_bytes(bool exact);  // k_bin_fast shared memory past the window
 cudaError_t launch_finalize(const Geom &g, const Accum &acc, Meta *meta_dev, int64_t n_rows_local,
                             int variant, cudaStream_t s);
 // bytes of shared memory per window bin

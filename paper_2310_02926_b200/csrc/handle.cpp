@@ -537,7 +537,8 @@ int bin_init(const bin_spec_t *spec, const bin_placement_t *place, const bin_com
     probe.nbins = B;
     // k_bin_fast (<= 1 attribute) keeps exact min/max in its window; the general kernel a filter
     const int bpb = spec->nattr <= 1 ? fast_window_bytes_per_bin(probe) : window_bytes_per_bin(probe);
-    const int qbytes = (spec->nattr <= 1 && B < (1ull << 29)) ? fast_queue_bytes() : 0;  // k_bin_fast queues
+    const int qbytes = (spec->nattr <= 1 && B < (1ull << 29)) ? fast_queue_bytes(spec->sum_mode == BIN_SUM_EXACT)
+                                                                : 0;  // k_bin_fast's exact-sum queues
     const int static_smem = 1024;  // kernels' static __shared__ (k_bin_fast: window-pick scratch)
     h->wcap = (h->lc.smem_optin - static_smem - qbytes) / bpb;
     h->smem_bytes = (int)((uint64_t)h->wcap >= B ? B * bpb : (uint64_t)h->wcap * bpb);
