@@ -228,7 +228,8 @@ typedef struct {
     int64_t bin_launches;     /* launches of the accumulate kernel */
     int32_t variant;          /* last accumulate variant (low 4 bits): 1 smem window + L2, 2 smem full grid,
                                  3 deterministic, 4 partition route; +16 when the single-attribute
-                                 k_bin_fast kernel ran, +32 when the NVLink peer combine ran */
+                                 k_bin_fast kernel ran, +32 when the NVLink peer combine ran,
+                                 +64 when it ran in the switch (NVLS, DATABIN_COMBINE=nvls) */
     int32_t window[BIN_MAX_DIM]; /* last window extents (bins), 0 = no window */
 } bin_profile_t;
 
