@@ -52,6 +52,9 @@ def parse():
     p.add_argument("--deterministic", action="store_true")
     p.add_argument("--exact", action="store_true", help="BIN_SUM_EXACT: correctly rounded exact sums (R20)")
     p.add_argument("--rows", type=int, default=0, help="experiments only: override the workload's total rows")
+    p.add_argument("--evolve", action="store_true",
+                   help="experiment: the inputs change every step (a KDK drift of every row on the bench stream "
+                        "before each execute); value = rows / the library's own per-execute device time")
     p.add_argument("--ops", default="", help="experiments only: comma list of ops instead of the workload's "
                                              "('none' = count only)")
     return p.parse_args()
@@ -307,7 +310,21 @@ def main():
     arrs = [db.wrap_tensor(cols[c], stream=stream.cuda_stream, mode=db.BIN_ASYNC) for c in list(w.axes) + list(w.attrs)]
     D = len(w.axes)
 
+    evolve_cols = None
+    if args.evolve:  # x, y (+ z, vx, vy, vz) drifted on the bench stream before every execute
+        extra = {}
+        for c in ("x", "y", "z", "vx", "vy", "vz"):
+            if c not in cols:
+                t = torch.empty(n, dtype=torch.float64, device=dev)
+                synth.fill_device(w.dist, w.central, w.seed, synth.COLUMNS[c], r0, n, t.data_ptr(), stream.cuda_stream)
+                extra[c] = t
+        torch.cuda.synchronize(dev)
+        allc = {**cols, **extra}
+        evolve_cols = [allc[c].data_ptr() for c in ("x", "y", "z", "vx", "vy", "vz")]
+
     def step():
+        if evolve_cols:
+            synth.kdk_step(evolve_cols, n, stream.cuda_stream, central_mass=0.0, dt=1e-3, start=r0)
         return db.bin_execute(h, arrs[:D], arrs[D:])
 
     # ---- warmup
@@ -392,6 +409,10 @@ def main():
         out_bytes = B * 8 * (1 + 4 * len(w.attrs))
         step_alg_bytes = bytes_per_row * N_total + out_bytes
         value = N_total / (ms_step * 1e-3)
+        if args.evolve:  # the step also ran the producer's KDK kernel: count the library's own phases only
+            lib_ms = sum(getattr(prof, "ms_" + k) for k in ("stage", "init", "bounds", "window", "bin", "combine",
+                                                            "finalize")) / max(1, prof.executes)
+            value = N_total / (lib_ms * 1e-3)
         var = int(prof.variant)
         D = len(w.axes)
         if var & 15 == 4:
@@ -420,6 +441,8 @@ def main():
                        "exec": "lockstep (BIN_EXEC_SYNC, stream-ordered)", "deterministic": args.deterministic,
                        "sum_mode": "exact (BIN_SUM_EXACT)" if args.exact else "fast",
                        "l2": "inputs 24 B/row x rows >> 126 MB L2; no flush needed",
+                       "inputs": ("evolving: a KDK drift of every row (synth.kdk_step, dt 1e-3) before every execute; "
+                                  "value from the library's per-execute phase times") if args.evolve else "fixed",
                        "parallelism": f"dp{world} (contiguous row shards per rank)", "combine": combine},
             "hbm": {"alg_bytes_per_step": step_alg_bytes,
                     "achieved_gbs_step": step_alg_bytes / (ms_step * 1e-3) / 1e9 / world,
