@@ -191,10 +191,17 @@ typedef struct {
                                0 = read in place; bin_inputs_released tells when the producer may overwrite */
 } bin_placement_t;
 
-/* Multi-rank combine: ranks bin their own rows and the bin
- * arrays are all-reduced with NCCL.  nccl_unique_id points at a 128-byte
- * ncclUniqueId created by bin_nccl_unique_id on rank 0 and broadcast by the
- * caller (NULL when nranks == 1). */
+/* Multi-rank combine: ranks bin their own rows and every rank
+ * receives the combined grid (reading R21).  nccl_unique_id points at a
+ * 128-byte ncclUniqueId created by bin_nccl_unique_id on rank 0 and broadcast
+ * by the caller (NULL when nranks == 1).  The combine is chosen at bin_init
+ * (environment variable DATABIN_COMBINE, which must be the same on every
+ * rank): default -- one kernel that reduces the rank's bin slice from every
+ * rank's accumulators over NVLink peer memory (CUDA IPC), finalizes it and
+ * writes it into every rank, when all ranks are on distinct GPUs of one node;
+ * "nvls" -- the same, reduced in the NVSwitch (multicast memory); "nccl" --
+ * NCCL allreduces + a finalize kernel (also the fallback when peer mapping
+ * fails).  Deterministic handles fold the ranks' sums in rank order. */
 typedef struct {
     int32_t rank, nranks;
     const void *nccl_unique_id;
@@ -300,8 +307,13 @@ int bin_init_group(const bin_spec_t *spec, const bin_placement_t *place, int32_t
  * own work stream (placement as bin_execute), then one launch combines and
  * finalizes all ranks after every rank has binned; each rank's result is then
  * available through bin_wait / bin_result on its own handle with the shared
- * *ticket.  Errors: as bin_execute; BIN_ESTATE when a handle is not rank r of
- * the group, was finalized, or the ranks' tickets differ. */
+ * *ticket.  The combine launch spins on barrier words inside the kernel, so it
+ * uses at most one CTA per SM in total and needs them co-resident: other work
+ * that fills every SM of the device at the same time can delay it past its
+ * ~2 s barrier timeout (reported as BIN_ENCCL at bin_wait, never a hang).
+ * Errors: as bin_execute; BIN_ESTATE when a handle is not rank r of the group,
+ * was finalized, or the ranks' tickets differ (e.g. after a failed group
+ * execute: the group must then be finalized and re-created). */
 int bin_execute_group(bin_handle_t *const *h, int32_t nranks, bin_array_t *const *axes, int32_t naxes,
                       bin_array_t *const *attrs, int32_t nattr, uint64_t *ticket);
 
