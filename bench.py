@@ -52,6 +52,8 @@ def parse():
     p.add_argument("--deterministic", action="store_true")
     p.add_argument("--exact", action="store_true", help="BIN_SUM_EXACT: correctly rounded exact sums (R20)")
     p.add_argument("--rows", type=int, default=0, help="experiments only: override the workload's total rows")
+    p.add_argument("--no-phase-events", action="store_true",
+                   help="experiment: no per-phase CUDA events inside the timed region (no roofline / phase times)")
     p.add_argument("--evolve", action="store_true",
                    help="experiment: the inputs change every step (a KDK drift of every row on the bench stream "
                         "before each execute); value = rows / the library's own per-execute device time")
@@ -336,7 +338,7 @@ def main():
     torch.cuda.synchronize(dev)
 
     # ---- timed region: exactly K steps, barrier + synchronize on both sides
-    db.bin_profile_enable(h, True)
+    db.bin_profile_enable(h, not args.no_phase_events)
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     if world > 1:
@@ -404,7 +406,7 @@ def main():
         peak, peak_src = load_peaks()
         bytes_per_row = 8 * (len(w.axes) + len(w.attrs))
         alg_bytes_launch = bytes_per_row * n           # the bin kernel reads every axis/attr column once
-        achieved = alg_bytes_launch / (ms_bin * 1e-3) / 1e9
+        achieved = alg_bytes_launch / (ms_bin * 1e-3) / 1e9 if ms_bin > 0 else 0.0
         B = int(res.nbins)
         out_bytes = B * 8 * (1 + 4 * len(w.attrs))
         step_alg_bytes = bytes_per_row * N_total + out_bytes
@@ -448,7 +450,7 @@ def main():
                     "achieved_gbs_step": step_alg_bytes / (ms_step * 1e-3) / 1e9 / world,
                     "frac_of_8TBps_step": step_alg_bytes / (ms_step * 1e-3) / 1e9 / world / NOMINAL_HBM_GBS},
             "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved,
-                         "peak": peak, "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
+                         "peak": peak, "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak if achieved else None,
                          "traffic": load_traffic(w.name), "ms_per_launch": ms_bin,
                          "alg_bytes_per_launch": alg_bytes_launch,
                          "share_of_step": ms_bin / ms_step if ms_step else None},
