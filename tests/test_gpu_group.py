@@ -168,3 +168,16 @@ def test_group_errors(db):
     finally:
         for h in hs:
             db.bin_finalize(h)
+
+
+@pytest.mark.slow
+def test_group_c3_full_size_4_ranks(db):
+    """The bench's multi-GPU configuration at full size on one B200: C3 (100M
+    Plummer rows, 512^2) as 4 ranks of 25M rows each, the same fused combine
+    body as `bench.py --gpus 4`, against the oracle's partition mode P = 4."""
+    import synth
+    from tests.gpu_util import workload_inputs
+    w = synth.CONFIGS["c3"]
+    axes, attrs = workload_inputs(w)
+    out = run_group(db, 4, "fast", res=tuple(w.res), lo=list(w.lo), hi=list(w.hi), cols=(axes, attrs))
+    assert out["n_in"] + out["n_out"] == w.n
