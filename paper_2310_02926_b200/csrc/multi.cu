@@ -156,10 +156,14 @@ struct MOpS {
     int32_t axc[3];
     int32_t atc[BIN_MAX_ATTR];
     int8_t sslot[BIN_MAX_ATTR], mslot[BIN_MAX_ATTR];  // sum / min-max slot of each attribute, -1 none
+    uint32_t desc[BIN_MAX_ATTR];  // packed: column | (sslot + 1) << 8 | (mslot + 1) << 16 (one shared load)
     int32_t ndim, nattr, ok;
 };
 
-__global__ void __launch_bounds__(MULTI_THREADS) k_multi_bin(MultiArgs a) {
+#ifndef BIN_MULTI_MINB
+#define BIN_MULTI_MINB 2
+#endif
+__global__ void __launch_bounds__(MULTI_THREADS, BIN_MULTI_MINB) k_multi_bin(MultiArgs a) {
     __shared__ MOpS so[MULTI_MAX_OPS];
     __shared__ double sv[MULTI_MAX_COLS][MULTI_THREADS];  // this CTA's rows, one column per line
     __shared__ unsigned s_in[MULTI_MAX_OPS], s_out[MULTI_MAX_OPS];
@@ -190,6 +194,7 @@ __global__ void __launch_bounds__(MULTI_THREADS) k_multi_bin(MultiArgs a) {
             const bool in = j < o.nattr;
             t.sslot[j] = (int8_t)(in && ((o.acc.sum_mask >> j) & 1u) ? ss++ : -1);
             t.mslot[j] = (int8_t)(in && ((o.acc.mm_mask >> j) & 1u) ? ms++ : -1);
+            t.desc[j] = (uint32_t)(o.atc[j] & 0xff) | ((uint32_t)(t.sslot[j] + 1) << 8) | ((uint32_t)(t.mslot[j] + 1) << 16);
         }
         s_in[threadIdx.x] = 0u;
         s_out[threadIdx.x] = 0u;
@@ -233,30 +238,37 @@ __global__ void __launch_bounds__(MULTI_THREADS) k_multi_bin(MultiArgs a) {
             // load can only let a reduction through, never skip a needed one):
             // ~1 reduction per row and instance instead of 2 x attributes
             // (BIN_MULTI_MM_FILTER=0: reduce every min/max unconditionally)
-            for (int j0 = 0; j0 < o.nattr; j0 += 8) {
+            // (each attribute's value and descriptor read from shared memory once)
+            ulonglong2 *const mmb = o.mm;
+            double *const sumb = o.sum;
+            long long *const xsb = o.xs;
+            const int na = o.nattr;
+            for (int j0 = 0; j0 < na; j0 += 8) {
                 ulonglong2 cur[8];
+                double v[8];
+                uint32_t ds[8];
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
                     const int j = j0 + u;
+                    ds[u] = j < na ? o.desc[j] : 0u;
+                    v[u] = j < na ? sv[ds[u] & 0xffu][threadIdx.x] : 0.0;
                     cur[u] = make_ulonglong2(~0ull, ~0ull);
-                    if (BIN_MULTI_MM_FILTER && j < o.nattr && o.mslot[j] >= 0)
-                        cur[u] = __ldcg(o.mm + (uint64_t)o.mslot[j] * B + b);
+                    if (BIN_MULTI_MM_FILTER && (ds[u] >> 16))
+                        cur[u] = __ldcg(mmb + (uint64_t)((ds[u] >> 16) - 1u) * B + b);
                 }
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
-                    const int j = j0 + u;
-                    if (j >= o.nattr || o.sslot[j] < 0) continue;
-                    const double v = sv[o.atc[j]][threadIdx.x];
-                    if (o.xs) xsum_add_double(o.xs, B, o.sslot[j], b, v, s_xr[k]);
-                    else red_add_f64(&o.sum[(uint64_t)o.sslot[j] * B + b], v);
+                    const uint32_t sl = (ds[u] >> 8) & 0xffu;
+                    if (!sl) continue;
+                    if (xsb) xsum_add_double(xsb, B, (int)sl - 1, b, v[u], s_xr[k]);
+                    else red_add_f64(&sumb[(uint64_t)(sl - 1u) * B + b], v[u]);
                 }
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
-                    const int j = j0 + u;
-                    if (j >= o.nattr || o.mslot[j] < 0) continue;
-                    const double v = sv[o.atc[j]][threadIdx.x];
-                    ulonglong2 *p = o.mm + (uint64_t)o.mslot[j] * B + b;
-                    const unsigned long long e = enc_total(v);
+                    const uint32_t ml = ds[u] >> 16;
+                    if (!ml) continue;
+                    ulonglong2 *p = mmb + (uint64_t)(ml - 1u) * B + b;
+                    const unsigned long long e = enc_total(v[u]);
                     if (e < cur[u].x) red_min_u64(&p->x, e);
                     if (~e < cur[u].y) red_min_u64(&p->y, ~e);
                 }
