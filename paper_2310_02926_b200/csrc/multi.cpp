@@ -293,7 +293,7 @@ int bin_multi_init(const bin_multi_op_t *ops, int32_t nops, int32_t ncols, const
     // costs one more read of the columns.
     {
         const char *env = getenv("DATABIN_MULTI_L2_MB");
-        const double budget = (env ? atof(env) : 48.0) * 1048576.0;
+        const double budget = (env ? atof(env) : 64.0) * 1048576.0;
         double acc = 0;
         m->groups.push_back(0);
         for (int k = 0; k < nops; ++k) {
