@@ -21,6 +21,7 @@
 // totalOrder encoding for min/max, the same finalize body (tail.cuh).
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "db_internal.h"
 #include "dev_common.cuh"
@@ -290,7 +291,8 @@ __global__ void __launch_bounds__(MULTI_THREADS, BIN_MULTI_MINB) k_multi_bin(Mul
 cudaError_t launch_multi_bin(const MultiArgs &a, const LaunchCfg &lc, cudaStream_t s) {
     if (a.n == 0 || a.k1 <= a.k0) return cudaSuccess;
     int64_t blocks = (a.n + MULTI_THREADS - 1) / MULTI_THREADS;
-    const int64_t cap = (int64_t)lc.sms * 5;  // 5 x 41 KB of shared memory per SM
+    static const int per_sm = getenv("DATABIN_MULTI_CTAS_PER_SM") ? atoi(getenv("DATABIN_MULTI_CTAS_PER_SM")) : 4;
+    const int64_t cap = (int64_t)lc.sms * per_sm;  // grid-stride CTAs (2 resident per SM at 116 registers)
     if (blocks > cap) blocks = cap;
     k_multi_bin<<<(unsigned)blocks, MULTI_THREADS, 0, s>>>(a);
     return cudaGetLastError();
