@@ -256,6 +256,8 @@ struct MultiOp {
     int32_t axc[3];
     int32_t atc[BIN_MAX_ATTR];
     int32_t nattr;
+    uint32_t *flt;  // min/max filter: [bin][chunk of 8 attributes][hi32(enc min), hi32(~enc max)] (64 B), or nullptr
+    int32_t nfc;    // filter chunks per bin (ceil(nattr / 8) when the instance has min/max, else 0)
 };
 struct MultiArgs {
     const double *col[MULTI_MAX_COLS];
@@ -264,6 +266,7 @@ struct MultiArgs {
     int32_t k0, k1;         // instances [k0, k1) of this accumulate launch (L2-sized group)
     uint32_t used_cols;     // columns any instance reads
     uint32_t bound_cols;    // columns some auto-bounded instance takes bounds of
+    int32_t use_flt;        // min/max filter lines on (off while rows are few per bin: nearly every row is a first touch)
     const MultiOp *ops;     // device array [nops]
 };
 cudaError_t launch_multi_init(const MultiArgs &a, uint64_t max_work, cudaStream_t s);

@@ -84,7 +84,8 @@ static int alloc_mslot(bin_multi *m, MSlot &S) {
     const int K = m->K;
     std::vector<uint64_t> B(K);
     std::vector<int> ns(K), nm(K);
-    uint64_t nc = 0, nsu = 0, nmm = 0, nout_mm = 0, nout_avg = 0, nxs = 0;
+    std::vector<int> nfc(K);
+    uint64_t nc = 0, nsu = 0, nmm = 0, nout_mm = 0, nout_avg = 0, nxs = 0, nflt = 0;
     for (int k = 0; k < K; ++k) {
         const bin_spec_t &sp = m->ops[k].spec;
         uint64_t b = 1;
@@ -96,6 +97,8 @@ static int alloc_mslot(bin_multi *m, MSlot &S) {
             if (sp.ops[a] & (BIN_OP_MIN | BIN_OP_MAX)) nm[k]++;
         }
         if (sp.sum_mode == BIN_SUM_EXACT) nxs += b * ns[k] * XD_DIGITS;
+        nfc[k] = nm[k] ? (sp.nattr + 7) / 8 : 0;
+        nflt += b * nfc[k] * 16;
         nc += b + 2;
         nsu += b * ns[k];
         nmm += 2 * b * nm[k];
@@ -115,6 +118,7 @@ static int alloc_mslot(bin_multi *m, MSlot &S) {
     const size_t o_scratch = o; o += al(256);
     const size_t o_xrange = o; o += al((size_t)K * 2 * BIN_MAX_ATTR * 4);
     const size_t o_xs = o; o += al(nxs * 8);
+    const size_t o_flt = o; o += al(nflt * 4);
     const size_t total = o;
     cudaError_t e = cudaMalloc(&S.base, total);
     if (e != cudaSuccess) {
@@ -138,7 +142,7 @@ static int alloc_mslot(bin_multi *m, MSlot &S) {
     S.meta_d = (Meta *)(b0 + o_meta);
     S.ops_d = (MultiOp *)(b0 + o_ops);
     S.ops_h.assign(K, MultiOp{});
-    uint64_t pc = 0, ps = 0, pm = 0, pomm = 0, poavg = 0, px = 0;
+    uint64_t pc = 0, ps = 0, pm = 0, pomm = 0, poavg = 0, px = 0, pf = 0;
     for (int k = 0; k < K; ++k) {
         const bin_multi_op_t &op = m->ops[k];
         MultiOp &t = S.ops_h[k];
@@ -175,6 +179,9 @@ static int alloc_mslot(bin_multi *m, MSlot &S) {
             acc.xrange = S.xrange + (size_t)k * 2 * BIN_MAX_ATTR;
             px += B[k] * ns[k] * XD_DIGITS;
         }
+        t.flt = nfc[k] ? (uint32_t *)(b0 + o_flt) + pf : nullptr;
+        t.nfc = nfc[k];
+        pf += B[k] * nfc[k] * 16;
         t.meta = S.meta_d + k;
         pc += B[k] + 2;
         ps += B[k] * ns[k];
@@ -286,14 +293,14 @@ int bin_multi_init(const bin_multi_op_t *ops, int32_t nops, int32_t ncols, const
     m->bound_cols = bound;
     m->max_work = max_work;
     m->max_bins = max_bins;
-    // Instances are accumulated in groups whose accumulators together fit an
-    // L2 budget: the reductions of one pass land in L2 only while the pass's
-    // working set stays resident (9 x 11.5 MB at once ran 2.2x slower than
-    // the same instances one after another).  Each extra group
-    // costs one more read of the columns.
+    // Instances are accumulated in groups whose hot lines (count, sums, min/max
+    // filter line) together fit an L2 budget: the reductions of one pass land
+    // in L2 only while the pass's working set stays resident (C6: 3 instances
+    // of 8 MiB per pass measured best).  Each extra group costs
+    // one more read of the columns.
     {
         const char *env = getenv("DATABIN_MULTI_L2_MB");
-        const double budget = (env ? atof(env) : 64.0) * 1048576.0;
+        const double budget = (env ? atof(env) : 24.0) * 1048576.0;
         double acc = 0;
         m->groups.push_back(0);
         for (int k = 0; k < nops; ++k) {
@@ -305,7 +312,9 @@ int bin_multi_init(const bin_multi_op_t *ops, int32_t nops, int32_t ncols, const
                 if (sp.ops[a2] & (BIN_OP_SUM | BIN_OP_AVG)) ns++;
                 if (sp.ops[a2] & (BIN_OP_MIN | BIN_OP_MAX)) nm++;
             }
-            const double bytes = B * (8.0 + 8.0 * ns + 16.0 * nm);
+            // hot per bin: count, sums and the min/max filter line (the min/max
+            // slots themselves are only touched by the rare improving rows)
+            const double bytes = B * (8.0 + 8.0 * ns + (nm ? 64.0 * ((sp.nattr + 7) / 8) : 0.0));
             if (k > m->groups.back() && acc + bytes > budget) {
                 m->groups.push_back(k);
                 acc = 0;
@@ -395,10 +404,17 @@ int bin_multi_execute(bin_multi_t *m, bin_array_t *const *cols, int32_t ncols, u
     if (S.xs && n >= (1ll << 30) / m->nranks)  // all ranks' rows < 2^30: digit headroom of the cross-rank add
         return set_error(BIN_EINVAL, "BIN_SUM_EXACT: %lld rows per execute and rank (limit 2^30 / %d ranks)",
                          (long long)n, m->nranks);
+    // min/max filter lines pay only once bins see several rows each: below
+    // that nearly every row is the first of its bin, passes the filter and
+    // would add the filter's own reductions to the slot's (then the lines are
+    // neither cleared nor read; measured crossover 4-15 rows per bin)
+    static const double flt_rpb = getenv("DATABIN_MULTI_FILTER_RPB") ? atof(getenv("DATABIN_MULTI_FILTER_RPB")) : 8.0;
+    const int use_flt = (double)n >= flt_rpb * (double)m->max_bins ? 1 : 0;
     {
         MultiArgs ai{};
         ai.nops = m->K;
         ai.ops = S.ops_d;
+        ai.use_flt = use_flt;
         if (had) DB_CUDA(cudaStreamWaitEvent(m->prep, S.done, 0));
         cudaError_t e0 = launch_multi_init(ai, m->max_work, m->prep);
         if (e0 != cudaSuccess) return cuda_error(e0, "multi init kernel");
@@ -499,6 +515,7 @@ int bin_multi_execute(bin_multi_t *m, bin_array_t *const *cols, int32_t ncols, u
         }
     }
     if ((rc = rec(MEV_BOUNDS, m->bound_cols != 0))) return rc;
+    a.use_flt = use_flt;
     // ---- a4 + a5 for all K: one pass over the rows per L2-sized group
     for (size_t gi = 0; gi + 1 < m->groups.size(); ++gi) {
         a.k0 = m->groups[gi];

@@ -45,6 +45,8 @@ __global__ void __launch_bounds__(MULTI_INIT_THREADS) k_multi_init(MultiArgs a) 
     const ulonglong2 ident = make_ulonglong2(~0ull, ~0ull);
     for (int64_t i = t0; i < (int64_t)(nb * acc.nmm); i += stride) ((ulonglong2 *)acc.mm)[i] = ident;
     if (t0 < 2 * o.g.ndim) acc.bounds[t0] = ~0ull;
+    if (o.flt && a.use_flt)
+        for (int64_t i = t0; i < (int64_t)(nb * o.nfc * 16); i += stride) o.flt[i] = ~0u;
     if (acc.xs) {  // exact sums: clear the digits of the slot's previous execute (range reset after)
         for (int s = 0; s < acc.nsum; ++s) {
             const int klo = acc.xrange[2 * s], khi = -acc.xrange[2 * s + 1];
@@ -131,9 +133,6 @@ cudaError_t launch_multi_bounds(const MultiArgs &a, const LaunchCfg &lc, cudaStr
 // compiler cannot prove they are global and atomicAdd/atomicMin become generic
 // returning ATOMs (one L2 round trip each; measured 2x slower than k_bin's
 // global path).  Explicit fire-and-forget global reductions instead:
-#ifndef BIN_MULTI_MM_FILTER
-#define BIN_MULTI_MM_FILTER 1
-#endif
 __device__ __forceinline__ void red_add_u64(unsigned long long *p, unsigned long long v) {
     asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(__cvta_generic_to_global(p)), "l"(v) : "memory");
 }
@@ -143,6 +142,15 @@ __device__ __forceinline__ void red_add_f64(double *p, double v) {
 __device__ __forceinline__ void red_min_u64(unsigned long long *p, unsigned long long v) {
     asm volatile("red.relaxed.gpu.global.min.u64 [%0], %1;" ::"l"(__cvta_generic_to_global(p)), "l"(v) : "memory");
 }
+__device__ __forceinline__ void red_min_u32(uint32_t *p, uint32_t v) {
+    asm volatile("red.relaxed.gpu.global.min.u32 [%0], %1;" ::"l"(__cvta_generic_to_global(p)), "r"(v) : "memory");
+}
+// 32 bytes of filter words in one L2 request (LDG.256, sm_100)
+__device__ __forceinline__ void ld_flt8(const uint32_t *p, uint32_t (&f)[8]) {
+    asm volatile("ld.relaxed.gpu.global.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(f[0]), "=r"(f[1]), "=r"(f[2]), "=r"(f[3]), "=r"(f[4]), "=r"(f[5]), "=r"(f[6]), "=r"(f[7])
+                 : "l"(__cvta_generic_to_global(p)));
+}
 
 // Instance table as the hot loop reads it (shared memory, warp-uniform reads).
 struct MOpS {
@@ -150,6 +158,7 @@ struct MOpS {
     unsigned long long *count;
     double *sum;
     ulonglong2 *mm;
+    uint32_t *flt;     // min/max filter lines (MultiOp::flt)
     long long *xs;     // BIN_SUM_EXACT digit rows (nullptr: fast sums)
     int32_t *xrange;
     uint64_t nbins;
@@ -158,7 +167,7 @@ struct MOpS {
     int32_t atc[BIN_MAX_ATTR];
     int8_t sslot[BIN_MAX_ATTR], mslot[BIN_MAX_ATTR];  // sum / min-max slot of each attribute, -1 none
     uint32_t desc[BIN_MAX_ATTR];  // packed: column | (sslot + 1) << 8 | (mslot + 1) << 16 (one shared load)
-    int32_t ndim, nattr, ok;
+    int32_t ndim, nattr, ok, nfc;
 };
 
 #ifndef BIN_MULTI_MINB
@@ -185,6 +194,8 @@ __global__ void __launch_bounds__(MULTI_THREADS, BIN_MULTI_MINB) k_multi_bin(Mul
         t.count = o.acc.count;
         t.sum = o.acc.sum;
         t.mm = (ulonglong2 *)o.acc.mm;
+        t.flt = o.flt;
+        t.nfc = o.nfc;
         t.xs = o.acc.xs;
         t.xrange = o.acc.xrange;
         t.nbins = o.acc.nbins;
@@ -232,30 +243,37 @@ __global__ void __launch_bounds__(MULTI_THREADS, BIN_MULTI_MINB) k_multi_bin(Mul
             DB_CHECK(b < o.nbins);
             red_add_u64(&o.count[b], 1ull);
             const uint64_t B = o.nbins;
-            // attributes in chunks of 8: the chunk's min/max slot pairs are loaded
-            // from L2 first, then the count / sum reductions are fired while the
-            // loads are in flight, and a min or max reduction is sent only when
-            // the row improves the loaded value (slots only decrease, so a stale
-            // load can only let a reduction through, never skip a needed one):
-            // ~1 reduction per row and instance instead of 2 x attributes
-            // (BIN_MULTI_MM_FILTER=0: reduce every min/max unconditionally)
+            // attributes in chunks of 8.  Min/max: a filter line per bin and chunk
+            // holds hi32(enc(min)) and hi32(~enc(max)) of every attribute (64 B,
+            // two LDG.256 = two L2 requests instead of one 16-B slot load per
+            // attribute); it is loaded first, the count / sum reductions are
+            // fired while the load is in flight, and a min or max reduction (plus
+            // the filter word's) is sent only when the row's hi32 is <= the loaded
+            // word.  Slots and filter words only decrease and a word is the hi32
+            // of a value already sent to its slot, so a skipped row's value is >
+            // a value the slot will hold: skipping never loses the extremum.
+            // Launches with MultiArgs::use_flt = 0 send every min/max reduction.
             // (each attribute's value and descriptor read from shared memory once)
             ulonglong2 *const mmb = o.mm;
             double *const sumb = o.sum;
             long long *const xsb = o.xs;
             const int na = o.nattr;
             for (int j0 = 0; j0 < na; j0 += 8) {
-                ulonglong2 cur[8];
+                uint32_t f[16];
                 double v[8];
                 uint32_t ds[8];
+                uint32_t *const fl = o.flt && a.use_flt ? o.flt + ((uint64_t)b * o.nfc + (j0 >> 3)) * 16 : nullptr;
+#pragma unroll
+                for (int u = 0; u < 16; ++u) f[u] = ~0u;
+                if (fl) {
+                    ld_flt8(fl, *reinterpret_cast<uint32_t(*)[8]>(&f[0]));
+                    if (na - j0 > 4) ld_flt8(fl + 8, *reinterpret_cast<uint32_t(*)[8]>(&f[8]));
+                }
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
                     const int j = j0 + u;
                     ds[u] = j < na ? o.desc[j] : 0u;
                     v[u] = j < na ? sv[ds[u] & 0xffu][threadIdx.x] : 0.0;
-                    cur[u] = make_ulonglong2(~0ull, ~0ull);
-                    if (BIN_MULTI_MM_FILTER && (ds[u] >> 16))
-                        cur[u] = __ldcg(mmb + (uint64_t)((ds[u] >> 16) - 1u) * B + b);
                 }
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
@@ -270,8 +288,15 @@ __global__ void __launch_bounds__(MULTI_THREADS, BIN_MULTI_MINB) k_multi_bin(Mul
                     if (!ml) continue;
                     ulonglong2 *p = mmb + (uint64_t)(ml - 1u) * B + b;
                     const unsigned long long e = enc_total(v[u]);
-                    if (e < cur[u].x) red_min_u64(&p->x, e);
-                    if (~e < cur[u].y) red_min_u64(&p->y, ~e);
+                    const uint32_t hn = (uint32_t)(e >> 32), hx = ~hn;
+                    if (hn <= f[2 * u]) {
+                        red_min_u64(&p->x, e);
+                        if (fl && hn < f[2 * u]) red_min_u32(fl + 2 * u, hn);
+                    }
+                    if (hx <= f[2 * u + 1]) {
+                        red_min_u64(&p->y, ~e);
+                        if (fl && hx < f[2 * u + 1]) red_min_u32(fl + 2 * u + 1, hx);
+                    }
                 }
             }
         }

@@ -245,3 +245,55 @@ def test_multi_repeated_executes_and_host_columns(db):
         db.bin_multi_finalize(m)
         for a in hs:
             db.bin_array_release(a)
+
+
+@pytest.mark.gpu
+def test_multi_filter_on_off_across_executes(db):
+    """The min/max filter lines (C6) are used only from 8 rows per bin
+    on: executes alternating below / above that (filter lines skipped, then
+    cleared and used, then skipped) on one handle all match the oracle."""
+    import torch
+    insts = paper_step_instances(64)[:4]  # 4096 bins: filter from 32,768 rows on
+    specs = [db.make_spec(d["res"], d["lo"], d["hi"], nattr=7) for d in insts]
+    m = db.bin_multi_init([db.make_multi_op(sp, d["axes"], d["attrs"]) for sp, d in zip(specs, insts)], 7,
+                          db.make_placement(device_id=0))
+    try:
+        for i, n in enumerate((20_000, 150_001, 3_000, 400_000, 150_001)):
+            cols = synth_cols(n, seed=40 + i, dist=i % 2)
+            ts = [torch.from_numpy(c).to("cuda:0") for c in cols]
+            hs = [db.wrap_tensor(t) for t in ts]
+            torch.cuda.synchronize()
+            try:
+                t = db.bin_multi_execute(m, hs)
+                for k, (d, sp) in enumerate(zip(insts, specs)):
+                    compare(db.result_to_numpy(m, t, sp, op=k), oracle_of(cols, d))
+            finally:
+                torch.cuda.synchronize()
+                for a in hs:
+                    db.bin_array_release(a)
+    finally:
+        db.bin_multi_finalize(m)
+
+
+@pytest.mark.gpu
+def test_multi_filter_hi32_ties(db):
+    """Values sharing their top 32 encoded bits (1 + k 2^-40, -(1 + k 2^-40))
+    in random order, 16 bins: the filter word ties on every row, so the exact
+    extremum must still reach the slot; min / max bit-exact vs the oracle."""
+    rng = np.random.default_rng(77)
+    n = 200_000
+    x = rng.uniform(-1, 1, n)
+    y = rng.uniform(-1, 1, n)
+    k = rng.permutation(n).astype(np.float64)
+    a = 1.0 + k * 2.0 ** -40
+    b = -(1.0 + rng.permutation(n) * 2.0 ** -40)
+    cols = [x, y, a, b]
+    insts = [dict(res=(4, 4), lo=(-1.0, -1.0), hi=(1.0, 1.0), axes=(0, 1), attrs=(2, 3)),
+             dict(res=(2, 2), lo=(-1.0, -1.0), hi=(1.0, 1.0), axes=(1, 0), attrs=(3, 2, 2))]
+    outs, _ = run_multi(db, cols, insts)
+    for d, out in zip(insts, outs):
+        ref = oracle_of(cols, d)
+        compare(out, ref)
+        for j in range(len(d["attrs"])):
+            assert np.array_equal(out["min"][j].view(np.uint64), ref["min"][j].view(np.uint64))
+            assert np.array_equal(out["max"][j].view(np.uint64), ref["max"][j].view(np.uint64))
