@@ -516,10 +516,16 @@ int bin_multi_execute(bin_multi_t *m, bin_array_t *const *cols, int32_t ncols, u
     }
     if ((rc = rec(MEV_BOUNDS, m->bound_cols != 0))) return rc;
     a.use_flt = use_flt;
-    // ---- a4 + a5 for all K: one pass over the rows per L2-sized group
-    for (size_t gi = 0; gi + 1 < m->groups.size(); ++gi) {
-        a.k0 = m->groups[gi];
-        a.k1 = m->groups[gi + 1];
+    // ---- a4 + a5 for all K: one pass over the rows per L2-sized group; with
+    // under ~3 rows per bin all K go in one pass (the lines are touched about
+    // once each, residency buys little, and the launch spreads the instances
+    // over grid.y: C6 at 46,875 rows 0.183 -> 0.160 ms, 131,072 0.275 -> 0.261)
+    static const double one_pass_rpb = getenv("DATABIN_MULTI_ONEPASS_RPB") ? atof(getenv("DATABIN_MULTI_ONEPASS_RPB")) : 3.0;
+    const bool one_pass = (double)n < one_pass_rpb * (double)m->max_bins;
+    const size_t ngroups = one_pass ? 1 : m->groups.size() - 1;
+    for (size_t gi = 0; gi < ngroups; ++gi) {
+        a.k0 = one_pass ? 0 : m->groups[gi];
+        a.k1 = one_pass ? m->K : m->groups[gi + 1];
         if ((e = launch_multi_bin(a, m->lc, s)) != cudaSuccess) return cuda_error(e, "multi bin kernel");
         if (n > 0) S.launches++;
     }

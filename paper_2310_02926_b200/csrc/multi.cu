@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(MULTI_THREADS, BIN_MULTI_MINB) k_multi_bin(Mul
 #pragma unroll
         for (int c = 0; c < MULTI_MAX_COLS; ++c)
             if ((a.used_cols >> c) & 1u) sv[c][threadIdx.x] = valid ? __ldcs(a.col[c] + i) : 0.0;
-        for (int k = 0; k < K; ++k) {
+        for (int k = blockIdx.y; k < K; k += gridDim.y) {  // (grid.y > 1: instances spread over CTAs, few rows)
             const MOpS &o = so[k];
             if (!o.ok) continue;
             bool in = valid;
@@ -317,9 +317,17 @@ cudaError_t launch_multi_bin(const MultiArgs &a, const LaunchCfg &lc, cudaStream
     if (a.n == 0 || a.k1 <= a.k0) return cudaSuccess;
     int64_t blocks = (a.n + MULTI_THREADS - 1) / MULTI_THREADS;
     static const int per_sm = getenv("DATABIN_MULTI_CTAS_PER_SM") ? atoi(getenv("DATABIN_MULTI_CTAS_PER_SM")) : 4;
-    const int64_t cap = (int64_t)lc.sms * per_sm;  // grid-stride CTAs (2 resident per SM at 116 registers)
+    const int64_t cap = (int64_t)lc.sms * per_sm;  // grid-stride CTAs (2 resident per SM at 94 registers)
     if (blocks > cap) blocks = cap;
-    k_multi_bin<<<(unsigned)blocks, MULTI_THREADS, 0, s>>>(a);
+    // too few rows to fill the machine: the group's instances go to separate
+    // CTAs (grid.y), each re-reading its rows' columns (from L2)
+    static const int ymax = getenv("DATABIN_MULTI_YMAX") ? atoi(getenv("DATABIN_MULTI_YMAX")) : 32;
+    int64_t y = (cap + blocks - 1) / blocks;
+    const int K = a.k1 - a.k0;
+    if (y > K) y = K;
+    if (y > ymax) y = ymax;
+    if (y < 1) y = 1;
+    k_multi_bin<<<dim3((unsigned)blocks, (unsigned)y), MULTI_THREADS, 0, s>>>(a);
     return cudaGetLastError();
 }
 
