@@ -1,5 +1,6 @@
 #!/usr/bin/env python
-"""k_bin_fast per-CTA phase trace (DATABIN_TRACE) at several row counts on one GPU -- diagnosis only."""
+"""k_bin_fast per-CTA phase trace (DATABIN_TRACE) at several row counts on one GPU -- diagnosis only.
+EXACT=1: the BIN_SUM_EXACT instantiation."""
 import os
 import sys
 
@@ -21,7 +22,8 @@ def main():
             synth.fill_device(w.dist, w.central, w.seed, synth.COLUMNS[c], 0, n, t.data_ptr(), 0)
             cols.append(t)
         torch.cuda.synchronize()
-        h = db.bin_init(db.make_spec(w.res, w.lo, w.hi, nattr=1), db.make_placement())
+        exact = os.environ.get("EXACT") == "1"
+        h = db.bin_init(db.make_spec(w.res, w.lo, w.hi, nattr=1, exact=exact), db.make_placement())
         hs = [db.wrap_tensor(t) for t in cols]
         print(f"--- n = {n:,}", file=sys.stderr, flush=True)
         for it in range(6):
