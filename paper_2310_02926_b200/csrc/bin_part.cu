@@ -679,10 +679,30 @@ __global__ void __launch_bounds__(PART_THREADS, 1) k_part_reduce(Accum acc, Part
             }
         }
         __syncthreads();
+        // a tile whose rows are all this CTA's (C4: ~16 whole tiles per CTA)
+        // is written with plain stores: no other CTA touches its bins, and
+        // k_prep left them at the identities (sums: load + add, since values
+        // outside the fixed range were already reduced into them above)
+        const bool owned = !XS && r0 == ts && r1 == te;
         for (uint32_t l = threadIdx.x; l < W; l += PART_THREADS) {
             const unsigned long long cnt = p_dsm[o_cnt + l];
             if (cnt == 0) continue;
             const uint64_t b = base + l;
+            if (owned) {
+                __stcg(&acc.count[b], cnt);
+#pragma unroll
+                for (int j = 0; j < A; ++j) {
+                    if (ss[j] >= 0) {
+                        const uint32_t w0 = o_fx + (uint32_t)ss[j] * 3u * W + l;
+                        const double d = fx_to_double(p_dsm[w0], p_dsm[w0 + W], p_dsm[w0 + 2 * W], cnt, fx[j].inv_scale);
+                        double *ps = &acc.sum[(uint64_t)ss[j] * B + b];
+                        if (d != 0.0) __stcg(ps, __ldcg(ps) + d);
+                    }
+                    if (ms[j] >= 0)
+                        __stcg((ulonglong2 *)acc.mm + (uint64_t)ms[j] * B + b, wmm[(uint32_t)ms[j] * W + l]);
+                }
+                continue;
+            }
             atomicAdd(&acc.count[b], cnt);
 #pragma unroll
             for (int j = 0; j < A; ++j) {
