@@ -21,6 +21,10 @@
 #include "dev_common.cuh"
 #include "xsum.cuh"
 
+#ifndef BIN_FAST_LD
+#define BIN_FAST_LD __ldcg
+#endif
+
 namespace db {
 
 extern __shared__ __align__(16) uint32_t f_dsm[];
@@ -357,8 +361,8 @@ __global__ void __launch_bounds__(FAST_THREADS, 1)
     double2 bx[D], bv = make_double2(0.0, 0.0);
     if (p0 < S) {
 #pragma unroll
-        for (int d = 0; d < D; ++d) bx[d] = __ldcs(cx[d] + p0);
-        if (A == 1) bv = __ldcs(cv + p0);
+        for (int d = 0; d < D; ++d) bx[d] = BIN_FAST_LD(cx[d] + p0);
+        if (A == 1) bv = BIN_FAST_LD(cv + p0);
     }
     const uint32_t W = c.W;
     c.o_fx = HM ? 2u * W : 0u;
@@ -386,8 +390,8 @@ __global__ void __launch_bounds__(FAST_THREADS, 1)
             double2 nx[D], nv = make_double2(0.0, 0.0);
             if (pn < S) {
 #pragma unroll
-                for (int d = 0; d < D; ++d) nx[d] = __ldcs(cx[d] + pn);
-                if (A == 1) nv = __ldcs(cv + pn);
+                for (int d = 0; d < D; ++d) nx[d] = BIN_FAST_LD(cx[d] + pn);
+                if (A == 1) nv = BIN_FAST_LD(cv + pn);
             }
 #ifdef BIN_FAST_LOADS_ONLY  // experiment: the streaming floor of this loop (rows consumed, nothing binned)
             {
@@ -426,8 +430,8 @@ __global__ void __launch_bounds__(FAST_THREADS, 1)
             uint32_t pc = base + lane;
             if (pc < npairs) {
 #pragma unroll
-                for (int d = 0; d < D; ++d) bx[d] = __ldcs(cx[d] + pc);
-                if (A == 1) bv = __ldcs(cv + pc);
+                for (int d = 0; d < D; ++d) bx[d] = BIN_FAST_LD(cx[d] + pc);
+                if (A == 1) bv = BIN_FAST_LD(cv + pc);
             }
             for (uint32_t i = 0; i < TAIL_Q; ++i, pc += 32) {
                 const bool valid = pc < npairs;
@@ -435,8 +439,8 @@ __global__ void __launch_bounds__(FAST_THREADS, 1)
                 double2 nx[D], nv = make_double2(0.0, 0.0);
                 if (i + 1 < TAIL_Q && pn < npairs) {
 #pragma unroll
-                    for (int d = 0; d < D; ++d) nx[d] = __ldcs(cx[d] + pn);
-                    if (A == 1) nv = __ldcs(cv + pn);
+                    for (int d = 0; d < D; ++d) nx[d] = BIN_FAST_LD(cx[d] + pn);
+                    if (A == 1) nv = BIN_FAST_LD(cv + pn);
                 }
                 double x[D];
 #pragma unroll

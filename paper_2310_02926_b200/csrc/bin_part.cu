@@ -101,6 +101,12 @@ __device__ __forceinline__ uint32_t part_key(const DGeom &G, const double (&x)[D
 }
 
 // ---------------------------------------------------------------- P1
+#ifndef PART_KEYS_LD
+#define PART_KEYS_LD __ldcg
+#endif
+#ifndef PART_RED_LD
+#define PART_RED_LD __ldcg
+#endif
 // Key slots: pair p (rows head+2p, head+2p+1) -> slots 2p, 2p+1; the
 // unpaired head row -> slot 2*npairs, the unpaired tail row -> 2*npairs+1.
 // Both belong to the last chunk.  Chunk c = pairs [npairs*c/C, npairs*(c+1)/C),
@@ -134,8 +140,8 @@ __global__ void __launch_bounds__(NT, 2) k_part_keys(Geom g, Inputs in, Accum ac
         double2 a[D], b[D];
 #pragma unroll
         for (int d = 0; d < D; ++d) {
-            a[d] = __ldcs(cx[d] + p);
-            b[d] = has2 ? __ldcs(cx[d] + q) : make_double2(0.0, 0.0);
+            a[d] = PART_KEYS_LD(cx[d] + p);
+            b[d] = has2 ? PART_KEYS_LD(cx[d] + q) : make_double2(0.0, 0.0);
         }
         double x[D];
 #pragma unroll
@@ -619,9 +625,9 @@ __global__ void __launch_bounds__(PART_THREADS, 1) k_part_reduce(Accum acc, Part
             for (int u = 0; u < U; ++u) {
                 const uint32_t i = i0 + u * PART_THREADS;
                 const bool ok = i < r1;
-                key[u] = ok ? __ldcs(pa.skey + i) : ~0u;
+                key[u] = ok ? PART_RED_LD(pa.skey + i) : ~0u;
 #pragma unroll
-                for (int j = 0; j < A; ++j) v[j][u] = (ok && j < nl) ? __ldcs(pa.sval + j * cap + i) : 0.0;
+                for (int j = 0; j < A; ++j) v[j][u] = (ok && j < nl) ? PART_RED_LD(pa.sval + j * cap + i) : 0.0;
             }
         };
         load(r0 + threadIdx.x);

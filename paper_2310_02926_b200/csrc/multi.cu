@@ -28,6 +28,10 @@
 #include "tail.cuh"
 #include "xsum.cuh"
 
+#ifndef MULTI_LD
+#define MULTI_LD __ldcg
+#endif
+
 namespace db {
 
 constexpr int MULTI_THREADS = 256;
@@ -221,7 +225,7 @@ __global__ void __launch_bounds__(MULTI_THREADS, BIN_MULTI_MINB) k_multi_bin(Mul
         // each used column of this row read once from HBM (only this thread reads its line)
 #pragma unroll
         for (int c = 0; c < MULTI_MAX_COLS; ++c)
-            if ((a.used_cols >> c) & 1u) sv[c][threadIdx.x] = valid ? __ldcs(a.col[c] + i) : 0.0;
+            if ((a.used_cols >> c) & 1u) sv[c][threadIdx.x] = valid ? MULTI_LD(a.col[c] + i) : 0.0;
         for (int k = blockIdx.y; k < K; k += gridDim.y) {  // (grid.y > 1: instances spread over CTAs, few rows)
             const MOpS &o = so[k];
             if (!o.ok) continue;
