@@ -199,9 +199,9 @@ __global__ void __launch_bounds__(GenThreads<A>::value, 1)
     auto row = [&](int64_t r) {
         double x[D], v[AA];
 #pragma unroll
-        for (int d = 0; d < D; ++d) x[d] = __ldcs(in.ax[d] + r);
+        for (int d = 0; d < D; ++d) x[d] = DB_LD_STREAM(in.ax[d] + r);
 #pragma unroll
-        for (int a = 0; a < A; ++a) v[a] = ((load_mask >> a) & 1u) ? __ldcs(in.at[a] + r) : 0.0;
+        for (int a = 0; a < A; ++a) v[a] = ((load_mask >> a) & 1u) ? DB_LD_STREAM(in.at[a] + r) : 0.0;
         accumulate_row<D, A, XS>(c, fx, x, v, n_in);
         ++rows_mine;
     };
@@ -211,10 +211,10 @@ __global__ void __launch_bounds__(GenThreads<A>::value, 1)
         double2 cx[D], cv[AA];
         auto load_pair = [&](int64_t q, double2 (&xx)[D], double2 (&vv)[AA]) {
 #pragma unroll
-            for (int d = 0; d < D; ++d) xx[d] = __ldcs((const double2 *)(in.ax[d] + head) + q);
+            for (int d = 0; d < D; ++d) xx[d] = DB_LD_STREAM((const double2 *)(in.ax[d] + head) + q);
 #pragma unroll
             for (int a = 0; a < A; ++a)
-                vv[a] = ((load_mask >> a) & 1u) ? __ldcs((const double2 *)(in.at[a] + head) + q) : make_double2(0.0, 0.0);
+                vv[a] = ((load_mask >> a) & 1u) ? DB_LD_STREAM((const double2 *)(in.at[a] + head) + q) : make_double2(0.0, 0.0);
         };
         if (tid < npairs) load_pair(tid, cx, cv);
         for (int64_t p = tid; p < npairs; p += nthr) {

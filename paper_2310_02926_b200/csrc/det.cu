@@ -45,8 +45,8 @@ __global__ void __launch_bounds__(256) k_det_keys(Geom g, Inputs in, Accum acc, 
         for (int u = 0; u < U; ++u) {
             const int64_t i = i0 + u * stride;
 #pragma unroll
-            for (int d = 0; d < 3; ++d) x[u][d] = (d < g.ndim && i < in.n) ? __ldcs(in.ax[d] + i) : 0.0;
-            v[u] = (VALS && i < in.n) ? __ldcs(in.at[va] + i) : 0.0;
+            for (int d = 0; d < 3; ++d) x[u][d] = (d < g.ndim && i < in.n) ? DB_LD_STREAM(in.ax[d] + i) : 0.0;
+            v[u] = (VALS && i < in.n) ? DB_LD_STREAM(in.at[va] + i) : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const uint32_t *keys, in
 #pragma unroll
     for (int j = 0; j < RS_ITEMS; ++j) {
         const int64_t i = base + j * RS_THREADS + threadIdx.x;
-        kk[j] = i < n ? __ldcs(keys + i) : ~0u;
+        kk[j] = i < n ? DB_LD_STREAM(keys + i) : ~0u;
     }
 #pragma unroll
     for (int j = 0; j < RS_ITEMS; ++j)
@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(RS_THREADS, 3) k_rs_scatter(const uint32_t *ke
 #pragma unroll
     for (int r = 0; r < RS_ITEMS; ++r) {
         const int64_t i = base + w * (32 * RS_ITEMS) + r * 32 + lane;
-        key[r] = i < n ? __ldcs(keys + i) : 0u;
+        key[r] = i < n ? DB_LD_STREAM(keys + i) : 0u;
     }
 #pragma unroll
     for (int r = 0; r < RS_ITEMS; ++r) {
@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(RS_THREADS, 3) k_rs_scatter(const uint32_t *ke
         const uint32_t idx = dstart[d] + wcnt[w][d] + lr[r];
         DB_CHECK(idx < (uint32_t)RS_TILE);
         skey[idx] = key[r];
-        spay[idx] = __ldcs(pay + i);
+        spay[idx] = DB_LD_STREAM(pay + i);
     }
     __syncthreads();
     const int64_t cnt = n - base < RS_TILE ? n - base : RS_TILE;
@@ -284,7 +284,7 @@ __global__ void k_det_segments(const uint32_t *keys, int64_t n, uint32_t B, uint
     for (int64_t j0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; j0 < n; j0 += stride) {
         uint32_t k[5];
         if (j0 + 4 <= n && (((uintptr_t)(keys + j0)) & 15u) == 0) {
-            const uint4 q = __ldcs((const uint4 *)(keys + j0));
+            const uint4 q = DB_LD_STREAM((const uint4 *)(keys + j0));
             k[0] = q.x, k[1] = q.y, k[2] = q.z, k[3] = q.w;
         } else {
 #pragma unroll
@@ -318,7 +318,7 @@ constexpr uint32_t DET_LONG = 256;
 
 template <bool VALS>
 __device__ __forceinline__ double det_val(const Inputs &in, const void *payload, int a, uint32_t j) {
-    if (VALS) return __ldcs((const double *)payload + j);
+    if (VALS) return DB_LD_STREAM((const double *)payload + j);
     return in.at[a][((const uint32_t *)payload)[j]];
 }
 

@@ -6,6 +6,13 @@
 
 #include "db_internal.h"
 
+// Streaming column loads: L2-cached (ld.global.cg).  The evict-first hint
+// (ld.global.cs) measured slower on every streaming kernel tried (C4 keys
+// 7.05 vs 5.8 ms, C3 k_bin_fast 0.565 vs 0.559 ms).
+#ifndef DB_LD_STREAM
+#define DB_LD_STREAM __ldcg
+#endif
+
 namespace db {
 
 // Checked build (-DDATABIN_CHECKED, tools/build_variants.py checked=DATABIN_CHECKED):

@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(512) k_bounds(Inputs in, unsigned long long *b
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < in.n; i += stride) {
 #pragma unroll
         for (int d = 0; d < D; ++d) {
-            double x = __ldcs(in.ax[d] + i);
+            double x = DB_LD_STREAM(in.ax[d] + i);
             if (x == x) {  // NaN rows do not define bounds
                 unsigned long long e = enc_total(x);
                 mn[d] = e < mn[d] ? e : mn[d];

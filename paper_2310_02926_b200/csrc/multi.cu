@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(512) k_multi_bounds(MultiArgs a) {
 #pragma unroll
         for (int c = 0; c < MULTI_MAX_COLS; ++c) {
             if (!((a.bound_cols >> c) & 1u)) continue;
-            const double x = __ldcs(a.col[c] + i);
+            const double x = DB_LD_STREAM(a.col[c] + i);
             if (x == x) {
                 const unsigned long long e = enc_total(x);
                 mn[c] = e < mn[c] ? e : mn[c];
