@@ -85,6 +85,11 @@ __device__ __forceinline__ uint32_t block_scan_excl(uint32_t *a, uint32_t n, uin
     return total;
 }
 
+__device__ __forceinline__ uint32_t udiv(uint32_t x, const UDiv &p) {
+    const uint32_t t = __umulhi(x, p.m);
+    return (t + ((x - t) >> p.s1)) >> p.s2;
+}
+
 // Bin index of one row (a4), or ~0u outside the mesh.
 template <int D>
 __device__ __forceinline__ uint32_t part_key(const DGeom &G, const double (&x)[D]) {
@@ -128,8 +133,8 @@ __global__ void __launch_bounds__(NT, 2) k_part_keys(Geom g, Inputs in, Accum ac
     auto one = [&](const double (&x)[D]) -> uint32_t {
         const uint32_t b = part_key<D>(G, x);
         if (b != ~0u) {
-            DB_CHECK(b / Wt < T && b < acc.nbins);
-            atomicAdd(&hist[b / Wt], 1u);
+            DB_CHECK(udiv(b, pa.wt_div) == b / Wt && b / Wt < T && b < acc.nbins);
+            atomicAdd(&hist[udiv(b, pa.wt_div)], 1u);
             ++n_in;
         }
         return b;
@@ -301,7 +306,7 @@ __global__ void __launch_bounds__(NT, 2) k_part_scatter(Inputs in, PartArgs pa) 
     const bool two = pa.G1 > 1;
     uint32_t *okey = two ? pa.xkey : pa.skey;
     double *oval = two ? pa.xval : pa.sval;
-    const uint32_t Wg = pa.Wt * pa.G1, ng = pa.T1;
+    const uint32_t ng = pa.T1;
     const uint32_t C = pa.C, c = blockIdx.x;
     const uint32_t p0 = (uint32_t)(((uint64_t)pa.npairs * c) / C), p1 = (uint32_t)(((uint64_t)pa.npairs * (c + 1)) / C);
     const uint2 *kin = (const uint2 *)pa.keys;
@@ -349,7 +354,7 @@ __global__ void __launch_bounds__(NT, 2) k_part_scatter(Inputs in, PartArgs pa) 
         }
 #pragma unroll
         for (int r = 0; r < 2 * PPT; ++r) {
-            g[r] = key[r] != ~0u ? key[r] / Wg : 0u;
+            g[r] = key[r] != ~0u ? udiv(key[r], pa.wg_div) : 0u;
             rk[r] = key[r] != ~0u ? atomicAdd(&bcnt[g[r]], 1u) : 0u;
         }
         __syncthreads();
@@ -387,7 +392,7 @@ __global__ void __launch_bounds__(NT, 2) k_part_scatter(Inputs in, PartArgs pa) 
         if (r >= 0) {
             const uint32_t key = pa.keys[2 * (uint64_t)pa.npairs + threadIdx.x];
             if (key != ~0u) {
-                const uint64_t gp = atomicAdd(&cur[key / Wg], 1u);
+                const uint64_t gp = atomicAdd(&cur[udiv(key, pa.wg_div)], 1u);
                 okey[gp] = key;
 #pragma unroll
                 for (int j = 0; j < A; ++j)
@@ -489,7 +494,7 @@ __global__ void __launch_bounds__(NT, 2) k_part_refine(PartArgs pa) {
         for (int q = 0; q < RPT; ++q) {
             const uint32_t li = q * NT + threadIdx.x;
             key[q] = cb0 + li < cb1 ? ((const uint32_t *)ib)[li] : ~0u;
-            g[q] = key[q] != ~0u ? key[q] / Wt - tb : 0u;
+            g[q] = key[q] != ~0u ? udiv(key[q], pa.wt_div) - tb : 0u;
             rk[q] = key[q] != ~0u ? atomicAdd(&bcnt[g[q]], 1u) : 0u;
         }
         __syncthreads();
@@ -823,6 +828,8 @@ bool part_plan(const Inputs &in, const Accum &acc, int ndim, int smem_optin, int
     pa->Wt = (uint32_t)((B + T - 1) / T);
     pa->G1 = T <= 64 ? 1u : (uint32_t)((T + 63) / 64);
     pa->T1 = (uint32_t)((T + pa->G1 - 1) / pa->G1);
+    pa->wt_div = udiv_make(pa->Wt);
+    pa->wg_div = udiv_make(pa->Wt * pa->G1);
     pa->head = (int)head;
     pa->npairs = (uint32_t)((in.n - head) / 2);
     pa->tail = ((in.n - head) & 1) ? 1 : 0;

@@ -159,6 +159,20 @@ int fast_window_bytes_per_bin(const Accum &acc);  // k_bin_fast's window (bin_fa
 
 // partition route (bin_part.cu): rows grouped by tile of Wt bins, then
 // accumulated tile by tile in shared memory
+// x / d for a divisor fixed per launch: t = umulhi(x, m), q = (t + ((x - t) >> s1)) >> s2
+// (the branch-free round-up method; exact for every 32-bit x and d >= 1)
+struct UDiv {
+    uint32_t m, s1, s2;
+};
+inline UDiv udiv_make(uint32_t d) {
+    uint32_t l = 0;
+    while (l < 32 && (1ull << l) < d) ++l;  // ceil(log2 d)
+    UDiv u;
+    u.m = (uint32_t)((((1ull << 32) * ((1ull << l) - d)) / d) + 1);
+    u.s1 = l < 1 ? l : 1;
+    u.s2 = l > 1 ? l - 1 : 0;
+    return u;
+}
 struct PartArgs {
     uint32_t *keys;    // [2*npairs + 2] bin index per row slot, ~0u outside
     uint32_t *cnt;     // [T][C] rows of chunk c in tile t -> exclusive prefix over c
@@ -174,6 +188,7 @@ struct PartArgs {
     int32_t head, tail;
     uint32_t Wt, T, C;  // bins per tile, tiles, chunks (CTAs of P1 and P3)
     uint32_t G1, T1;    // tiles per super-tile (1: one level), super-tiles
+    UDiv wt_div, wg_div;  // / Wt and / (Wt * G1)
     int32_t nl;         // attributes read (<= 4) and which
     int32_t lattr[4];
 };
