@@ -784,7 +784,10 @@ int part_bytes_per_bin(const Accum &acc) { return 4 + 12 * acc.nsum + 16 * acc.n
 constexpr int SC_THREADS = 512;
 template <int A> struct PartCfg {
     static constexpr int PPT = A <= 1 ? 2 : 1;  // scatter: pairs per thread per batch
-    static constexpr int RPT = A <= 1 ? 4 : 2;  // refine: rows per thread per batch
+#ifndef PART_RPT1
+#define PART_RPT1 5
+#endif
+    static constexpr int RPT = A <= 1 ? PART_RPT1 : 2;  // refine: rows per thread per batch
 };
 static size_t scatter_smem(int A, int ppt) {
     const size_t NP = (size_t)ppt * SC_THREADS, R = 2 * NP;
