@@ -838,7 +838,7 @@ bool part_plan(const Inputs &in, const Accum &acc, int ndim, int smem_optin, int
     pa->tail = ((in.n - head) & 1) ? 1 : 0;
     pa->C = 2 * (uint32_t)sms;  // chunks: two 512-thread CTAs per SM in P1 and P3
     const int A = a_class(nl);
-    if ((int64_t)scatter_smem(A, A <= 1 ? 2 : 1) > avail || (int64_t)refine_smem(A, A <= 1 ? 4 : 2) > avail ||
+    if ((int64_t)scatter_smem(A, A <= 1 ? 2 : 1) > avail || (int64_t)refine_smem(A, A <= 1 ? PART_RPT1 : 2) > avail ||
         (int64_t)reduce_smem(acc, *pa) > avail || (int64_t)T * 4 + 33 * 4 > avail ||
         (int64_t)(pa->C + 1 + 33) * 4 > avail)
         return false;
