@@ -413,7 +413,8 @@ __global__ void __launch_bounds__(NT, 2) k_part_scatter(Inputs in, PartArgs pa) 
 template <int A, int RPT, int NT>
 __global__ void __launch_bounds__(NT, 2) k_part_refine(PartArgs pa) {
     constexpr int R = RPT * NT;
-    constexpr size_t IN_BYTES = (size_t)R * (4 + 8 * A);
+    constexpr int RS = R + 4;  // input slots: the batch from its row rounded down to a multiple of 4
+    constexpr size_t IN_BYTES = (size_t)RS * (4 + 8 * A);
     unsigned char *sm = (unsigned char *)p_dsm;
     double *st_val = (double *)(sm + 2 * IN_BYTES);
     uint32_t *st_key = (uint32_t *)(st_val + A * R);
@@ -457,16 +458,31 @@ __global__ void __launch_bounds__(NT, 2) k_part_refine(PartArgs pa) {
         n_b0 = b1;
         return true;
     };
+    // 16-byte copies of aligned groups of 4 rows (slot s = row - (b0 & ~3));
+    // the batch's partial first and last groups row by row (cap is a multiple of 4)
     auto issue = [&](int buf, uint32_t b0, uint32_t b1) {
         unsigned char *ib = sm + buf * IN_BYTES;
-#pragma unroll
-        for (int q = 0; q < RPT; ++q) {
-            const uint32_t li = q * NT + threadIdx.x, i = b0 + li;
-            if (i < b1) {
-                cp_async<4>(ib + (size_t)li * 4, pa.xkey + i);
+        const uint32_t base = b0 & ~3u, ng = (b1 - base + 3u) >> 2;
+        for (uint32_t gi = threadIdx.x; gi < ng; gi += NT) {
+            const uint32_t r0 = base + 4u * gi, s0 = 4u * gi;
+            if (r0 >= b0 && r0 + 4u <= b1) {
+                cp_async<16>(ib + (size_t)s0 * 4, pa.xkey + r0);
 #pragma unroll
                 for (int j = 0; j < A; ++j)
-                    if (j < nl) cp_async<8>(ib + (size_t)R * 4 + ((size_t)j * R + li) * 8, pa.xval + j * cap + i);
+                    if (j < nl) {
+                        unsigned char *vd = ib + (size_t)RS * 4 + ((size_t)j * RS + s0) * 8;
+                        cp_async<16>(vd, pa.xval + j * cap + r0);
+                        cp_async<16>(vd + 16, pa.xval + j * cap + r0 + 2);
+                    }
+            } else {
+                for (uint32_t u = 0; u < 4u; ++u) {
+                    const uint32_t i = r0 + u;
+                    if (i < b0 || i >= b1) continue;
+                    cp_async<4>(ib + (size_t)(s0 + u) * 4, pa.xkey + i);
+#pragma unroll
+                    for (int j = 0; j < A; ++j)
+                        if (j < nl) cp_async<8>(ib + (size_t)RS * 4 + ((size_t)j * RS + s0 + u) * 8, pa.xval + j * cap + i);
+                }
             }
         }
         cp_async_commit();
@@ -488,12 +504,14 @@ __global__ void __launch_bounds__(NT, 2) k_part_refine(PartArgs pa) {
             loaded_it = cit;
         }
         cp_async_wait1();
+        __syncthreads();  // (slots are filled by other threads' copies now)
         const unsigned char *ib = sm + (k & 1) * IN_BYTES;
+        const uint32_t off = cb0 & 3u;
         uint32_t key[RPT], g[RPT], rk[RPT];
 #pragma unroll
         for (int q = 0; q < RPT; ++q) {
             const uint32_t li = q * NT + threadIdx.x;
-            key[q] = cb0 + li < cb1 ? ((const uint32_t *)ib)[li] : ~0u;
+            key[q] = cb0 + li < cb1 ? ((const uint32_t *)ib)[off + li] : ~0u;
             g[q] = key[q] != ~0u ? udiv(key[q], pa.wt_div) - tb : 0u;
             rk[q] = key[q] != ~0u ? atomicAdd(&bcnt[g[q]], 1u) : 0u;
         }
@@ -508,7 +526,7 @@ __global__ void __launch_bounds__(NT, 2) k_part_refine(PartArgs pa) {
             st_key[pos] = key[q];
             st_g[pos] = (uint8_t)g[q];
 #pragma unroll
-            for (int j = 0; j < A; ++j) st_val[j * R + pos] = ((const double *)(ib + (size_t)R * 4))[(size_t)j * R + li];
+            for (int j = 0; j < A; ++j) st_val[j * R + pos] = ((const double *)(ib + (size_t)RS * 4))[(size_t)j * RS + off + li];
         }
         __syncthreads();
         const uint32_t nst = *nstp;
@@ -795,7 +813,7 @@ static size_t scatter_smem(int A, int ppt) {
 }
 static size_t refine_smem(int A, int rpt) {
     const size_t R = (size_t)rpt * SC_THREADS;
-    return 2 * R * (4 + 8 * (size_t)A) + R * (8 * (size_t)A + 4 + 1) + (4 * 128 + 4) * 4;
+    return 2 * (R + 4) * (4 + 8 * (size_t)A) + R * (8 * (size_t)A + 4 + 1) + (4 * 128 + 4) * 4;
 }
 static size_t reduce_smem(const Accum &acc, const PartArgs &pa) {
     const size_t win = (size_t)pa.Wt * part_bytes_per_bin(acc), eh = (size_t)(pa.nl > 0 ? pa.nl : 1) * 2048 * 4;

@@ -125,10 +125,11 @@ static int probe_route(const int32_t *p) {
 
 // Carves the partition scratch (256-byte aligned pieces): keys [n+2] |
 // cnt [T*C] | tot [T] | tstart [T+1] | off1 [T1*(C+1)] | skey [n] |
-// sval [nl][n] | (two-level) xkey [n] | xval [nl][n].
+// sval [nl][cap] | (two-level) xkey [n] | xval [nl][cap], cap = n rounded up to 4.
 static int ensure_part_scratch(bin_handle *h, int64_t n, PartArgs &pa) {
     auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
     const size_t nv = (size_t)(pa.nl > 0 ? pa.nl : 1);
+    const uint64_t capn = ((uint64_t)n + 3) & ~(uint64_t)3;  // value planes 32-byte aligned (refine's 16-byte copies)
     size_t o = 0;
     const size_t o_keys = o; o += al(((size_t)n + 2) * 4);
     const size_t o_cnt = o; o += al((size_t)pa.T * pa.C * 4);
@@ -136,9 +137,9 @@ static int ensure_part_scratch(bin_handle *h, int64_t n, PartArgs &pa) {
     const size_t o_ts = o; o += al(((size_t)pa.T + 1) * 4);
     const size_t o_off1 = o; o += al((size_t)pa.T1 * (pa.C + 1) * 4);
     const size_t o_skey = o; o += al((size_t)n * 4);
-    const size_t o_sval = o; o += al((size_t)n * 8 * nv);
+    const size_t o_sval = o; o += al((size_t)capn * 8 * nv);
     const size_t o_xkey = o; if (pa.G1 > 1) o += al((size_t)n * 4);
-    const size_t o_xval = o; if (pa.G1 > 1) o += al((size_t)n * 8 * nv);
+    const size_t o_xval = o; if (pa.G1 > 1) o += al((size_t)capn * 8 * nv);
     const size_t total = o;
     if (total > h->part_bytes) {
         if (h->part_base) {
@@ -166,7 +167,7 @@ static int ensure_part_scratch(bin_handle *h, int64_t n, PartArgs &pa) {
     pa.sval = (double *)(h->part_base + o_sval);
     pa.xkey = (uint32_t *)(h->part_base + o_xkey);
     pa.xval = (double *)(h->part_base + o_xval);
-    pa.cap = (uint64_t)n;
+    pa.cap = capn;
     return BIN_OK;
 }
 

@@ -1,0 +1,8 @@
+#!/bin/bash
+# refine 16-byte copies A/B (experiments only)
+export DATABIN_NO_BUILD=1
+timeout 900 python -m pytest tests/test_gpu_partition.py tests/test_gpu_parity.py tests/test_gpu_group.py tests/test_gpu_exact.py -q -x -p no:cacheprovider 2>&1 | tail -1
+for v in default head; do
+  [ $v = default ] && unset DATABIN_LIB || export DATABIN_LIB=paper_2310_02926_b200/variants/$v.so
+  for rep in 1 2; do echo "$v $(DATABIN_PART_TIMING=1 timeout 300 python bench.py --workload c4 --steps 5 --warmup 2 --no-e2e --no-cpu-baseline 2>&1 | grep -E 'part timing' | cut -c30-)"; done
+done
