@@ -116,13 +116,33 @@ __device__ __forceinline__ uint32_t part_key(const DGeom &G, const double (&x)[D
 // unpaired head row -> slot 2*npairs, the unpaired tail row -> 2*npairs+1.
 // Both belong to the last chunk.  Chunk c = pairs [npairs*c/C, npairs*(c+1)/C),
 // the same in P1 and P3.  Writes cnt[t*C + c] = rows of chunk c in tile t.
+// PART_KEYS_TMA: the chunk's axis columns are staged into shared memory by
+// TMA bulk copies (cp.async.bulk, one mbarrier per buffer, two buffers of
+// KEYS_SP pairs per column), so the loads in flight cost no registers.
+#ifndef PART_KEYS_TMA
+#define PART_KEYS_TMA 1
+#endif
+constexpr uint32_t KEYS_SP = 1024;  // pairs per stage and column (16 KB)
+__device__ __forceinline__ void keys_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src), "r"(bytes),
+                 "r"((unsigned)__cvta_generic_to_shared(bar))
+                 : "memory");
+}
+size_t keys_smem(int D, uint32_t T) { return (PART_KEYS_TMA ? 2ull * D * KEYS_SP * 16 : 0ull) + (size_t)T * 4; }
+
 template <int D, int NT>
 __global__ void __launch_bounds__(NT, 2) k_part_keys(Geom g, Inputs in, Accum acc, PartArgs pa) {
+#if PART_KEYS_TMA
+    const double2 *stage = (const double2 *)p_dsm;         // [2][D][KEYS_SP]
+    uint32_t *hist = p_dsm + (2u * D * KEYS_SP * 16u) / 4u;  // [T]
+    __shared__ __align__(8) uint64_t kbar[2];
+#else
     uint32_t *hist = p_dsm;  // [T]
+#endif
     const DGeom G = load_geom<D>(g, acc.bounds);
     const uint32_t T = pa.T, C = pa.C, c = blockIdx.x;
     for (uint32_t i = threadIdx.x; i < T; i += NT) hist[i] = 0u;
-    __syncthreads();
     const uint32_t p0 = (uint32_t)(((uint64_t)pa.npairs * c) / C), p1 = (uint32_t)(((uint64_t)pa.npairs * (c + 1)) / C);
     const double2 *cx[D];
 #pragma unroll
@@ -139,6 +159,59 @@ __global__ void __launch_bounds__(NT, 2) k_part_keys(Geom g, Inputs in, Accum ac
         }
         return b;
     };
+#if PART_KEYS_TMA
+    const uint32_t nst = (p1 - p0 + KEYS_SP - 1) / KEYS_SP;
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < 2; ++b)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((unsigned)__cvta_generic_to_shared(&kbar[b]))
+                         : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();  // (also: hist zeroed)
+    auto issue = [&](uint32_t k) {  // thread 0: stage k into buffer k & 1
+        const uint32_t ps = p0 + k * KEYS_SP, np = min(KEYS_SP, p1 - ps);
+        uint64_t *bar = &kbar[k & 1u];
+        unsigned long long st;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 %0, [%1], %2;"
+                     : "=l"(st) : "r"((unsigned)__cvta_generic_to_shared(bar)), "r"((unsigned)(D * np * 16u)) : "memory");
+        (void)st;
+#pragma unroll
+        for (int d = 0; d < D; ++d)
+            keys_g2s((void *)(stage + ((k & 1u) * D + d) * KEYS_SP), cx[d] + ps, np * 16u, bar);
+    };
+    if (threadIdx.x == 0) {
+        if (nst > 0) issue(0);
+        if (nst > 1) issue(1);
+    }
+    for (uint32_t k = 0; k < nst; ++k) {
+        {
+            const unsigned bar = (unsigned)__cvta_generic_to_shared(&kbar[k & 1u]), par = (k >> 1) & 1u;
+            unsigned done = 0;
+            while (!done)
+                asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                             : "=r"(done) : "r"(bar), "r"(par) : "memory");
+        }
+        const uint32_t ps = p0 + k * KEYS_SP, np = min(KEYS_SP, p1 - ps);
+        const double2 *sb = stage + (k & 1u) * D * KEYS_SP;
+        for (uint32_t li = threadIdx.x; li < np; li += NT) {
+            double2 a[D];
+#pragma unroll
+            for (int d = 0; d < D; ++d) a[d] = sb[d * KEYS_SP + li];
+            double x[D];
+#pragma unroll
+            for (int d = 0; d < D; ++d) x[d] = a[d].x;
+            const uint32_t k0 = one(x);
+#pragma unroll
+            for (int d = 0; d < D; ++d) x[d] = a[d].y;
+            const uint32_t k1 = one(x);
+            __stcg(kout + ps + li, make_uint2(k0, k1));
+            rows += 2;
+        }
+        __syncthreads();  // buffer k & 1 read by every thread
+        if (threadIdx.x == 0 && k + 2 < nst) issue(k + 2);
+    }
+#else
+    __syncthreads();
     for (uint32_t p = p0 + threadIdx.x; p < p1; p += 2 * NT) {
         const uint32_t q = p + NT;
         const bool has2 = q < p1;
@@ -168,6 +241,7 @@ __global__ void __launch_bounds__(NT, 2) k_part_keys(Geom g, Inputs in, Accum ac
             rows += 2;
         }
     }
+#endif
     if (c == C - 1 && threadIdx.x < 2) {  // unpaired head / tail row
         const int64_t r = threadIdx.x == 0 ? (pa.head ? 0 : -1) : (pa.tail ? in.n - 1 : -1);
         if (r >= 0) {
@@ -857,7 +931,7 @@ bool part_plan(const Inputs &in, const Accum &acc, int ndim, int smem_optin, int
     pa->C = 2 * (uint32_t)sms;  // chunks: two 512-thread CTAs per SM in P1 and P3
     const int A = a_class(nl);
     if ((int64_t)scatter_smem(A, A <= 1 ? 2 : 1) > avail || (int64_t)refine_smem(A, A <= 1 ? PART_RPT1 : 2) > avail ||
-        (int64_t)reduce_smem(acc, *pa) > avail || (int64_t)T * 4 + 33 * 4 > avail ||
+        (int64_t)reduce_smem(acc, *pa) > avail || (int64_t)keys_smem(ndim, (uint32_t)T) + 33 * 4 > avail ||
         (int64_t)(pa->C + 1 + 33) * 4 > avail)
         return false;
     return true;
@@ -865,7 +939,7 @@ bool part_plan(const Inputs &in, const Accum &acc, int ndim, int smem_optin, int
 
 template <int D>
 static cudaError_t launch_keys_d(const Geom &g, const Inputs &in, const Accum &acc, const PartArgs &pa, cudaStream_t s) {
-    const size_t smem = (size_t)pa.T * 4;
+    const size_t smem = keys_smem(D, pa.T);
     auto k = k_part_keys<D, SC_THREADS>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
