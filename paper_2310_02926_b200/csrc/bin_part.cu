@@ -370,7 +370,11 @@ __device__ __forceinline__ void claim_ranges(uint32_t *bcnt, uint32_t *boff, uin
 template <int A, int PPT, int NT>
 __global__ void __launch_bounds__(NT, 2) k_part_scatter(Inputs in, PartArgs pa) {
     constexpr int NP = PPT * NT, R = 2 * NP;
-    constexpr size_t IN_BYTES = (size_t)NP * (8 + 16 * A);
+    // input buffers: keys uint2 [NP + 2] (bulk copy from the batch's first pair
+    // rounded down to even, so source and size are 16-byte multiples) | vals double2 [A][NP]
+    constexpr size_t KB = (size_t)(NP + 2) * 8;
+    constexpr size_t IN_BYTES = KB + (size_t)NP * 16 * A;
+    __shared__ __align__(8) uint64_t sbar[2];
     unsigned char *sm = (unsigned char *)p_dsm;
     double *st_val = (double *)(sm + 2 * IN_BYTES);
     uint32_t *st_key = (uint32_t *)(st_val + A * R);
@@ -390,21 +394,29 @@ __global__ void __launch_bounds__(NT, 2) k_part_scatter(Inputs in, PartArgs pa) 
     for (int j = 0; j < A; ++j) cv[j] = (const double2 *)(in.at[pa.lattr[j < nl ? j : 0]] + pa.head);
     const uint64_t cap = pa.cap;
     const uint32_t nb = (p1 - p0 + NP - 1) / NP;
+    // TMA bulk copies of batch k into buffer k & 1 (thread 0; one mbarrier per buffer)
     auto issue = [&](uint32_t k) {
         unsigned char *ib = sm + (k & 1) * IN_BYTES;
+        const uint32_t ps = p0 + k * NP, np = min((uint32_t)NP, p1 - ps);
+        const uint32_t kbase = ps & ~1u, nkp = (ps + np - kbase + 1u) & ~1u;  // <= npairs + 1 slots: in bounds
+        uint64_t *bar = &sbar[k & 1];
+        unsigned long long st;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 %0, [%1], %2;"
+                     : "=l"(st) : "r"((unsigned)__cvta_generic_to_shared(bar)), "r"(nkp * 8u + (uint32_t)nl * np * 16u)
+                     : "memory");
+        (void)st;
+        keys_g2s(ib, kin + kbase, nkp * 8u, bar);
 #pragma unroll
-        for (int q = 0; q < PPT; ++q) {
-            const uint32_t li = q * NT + threadIdx.x, p = p0 + k * NP + li;
-            if (p < p1) {
-                cp_async<8>(ib + (size_t)li * 8, kin + p);
-#pragma unroll
-                for (int j = 0; j < A; ++j)
-                    if (j < nl) cp_async<16>(ib + (size_t)NP * 8 + ((size_t)j * NP + li) * 16, cv[j] + p);
-            }
-        }
-        cp_async_commit();
+        for (int j = 0; j < A; ++j)
+            if (j < nl) keys_g2s(ib + KB + (size_t)j * NP * 16, cv[j] + ps, np * 16u, bar);
     };
-    if (nb > 0) issue(0);
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < 2; ++b)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((unsigned)__cvta_generic_to_shared(&sbar[b]))
+                         : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        if (nb > 0) issue(0);
+    }
     if (threadIdx.x < 128) {
         bcnt[threadIdx.x] = 0u;
         const uint32_t gi = threadIdx.x;
@@ -414,15 +426,22 @@ __global__ void __launch_bounds__(NT, 2) k_part_scatter(Inputs in, PartArgs pa) 
     }
     __syncthreads();
     for (uint32_t k = 0; k < nb; ++k) {
-        if (k + 1 < nb) issue(k + 1);
-        else cp_async_commit();
-        cp_async_wait1();  // this thread's copies of batch k have landed
+        if (threadIdx.x == 0 && k + 1 < nb) issue(k + 1);  // (buffer (k+1)&1 was last read before this
+                                                            //  iteration's barriers of batch k-1)
+        {
+            const unsigned bar = (unsigned)__cvta_generic_to_shared(&sbar[k & 1]), par = (k >> 1) & 1u;
+            unsigned done = 0;
+            while (!done)
+                asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                             : "=r"(done) : "r"(bar), "r"(par) : "memory");
+        }
         const unsigned char *ib = sm + (k & 1) * IN_BYTES;
+        const uint32_t koff = (p0 + k * NP) & 1u;
         uint32_t key[2 * PPT], g[2 * PPT], rk[2 * PPT];
 #pragma unroll
         for (int q = 0; q < PPT; ++q) {
             const uint32_t li = q * NT + threadIdx.x;
-            const uint2 kk = (p0 + k * NP + li < p1) ? ((const uint2 *)ib)[li] : make_uint2(~0u, ~0u);
+            const uint2 kk = (p0 + k * NP + li < p1) ? ((const uint2 *)ib)[koff + li] : make_uint2(~0u, ~0u);
             key[2 * q] = kk.x;
             key[2 * q + 1] = kk.y;
         }
@@ -443,7 +462,7 @@ __global__ void __launch_bounds__(NT, 2) k_part_scatter(Inputs in, PartArgs pa) 
             st_g[pos] = (uint8_t)g[r];
 #pragma unroll
             for (int j = 0; j < A; ++j) {
-                const double2 v = ((const double2 *)(ib + (size_t)NP * 8))[(size_t)j * NP + li];
+                const double2 v = ((const double2 *)(ib + KB))[(size_t)j * NP + li];
                 st_val[j * R + pos] = (r & 1) ? v.y : v.x;
             }
         }
@@ -883,7 +902,7 @@ template <int A> struct PartCfg {
 };
 static size_t scatter_smem(int A, int ppt) {
     const size_t NP = (size_t)ppt * SC_THREADS, R = 2 * NP;
-    return 2 * NP * (8 + 16 * (size_t)A) + R * (8 * (size_t)A + 4 + 1) + (4 * 128 + 4) * 4;
+    return 2 * ((NP + 2) * 8 + NP * 16 * (size_t)A) + R * (8 * (size_t)A + 4 + 1) + (4 * 128 + 4) * 4;
 }
 static size_t refine_smem(int A, int rpt) {
     const size_t R = (size_t)rpt * SC_THREADS;
