@@ -10,7 +10,7 @@
 //   P2 k_part_scan1/2  per-tile prefix over chunks, tile starts and the
 //                      per-(group, chunk) write offsets: every output position
 //                      is known before the scatter (no L2 atomic claims)
-//   P3 k_part_scatter  read keys + attributes (cp.async double buffer),
+//   P3 k_part_scatter  read keys + attributes (TMA bulk copies, double buffer),
 //                      counting-sort each batch of rows by group in shared
 //                      memory, write the rows out as contiguous runs at the
 //                      offsets of P2 (coalesced).
@@ -315,17 +315,6 @@ __global__ void __launch_bounds__(1024) k_part_scan2(PartArgs pa) {
     if (threadIdx.x == 0) pa.tstart[T] = total;
 }
 
-// ---------------------------------------------------------------- cp.async
-template <int N>
-__device__ __forceinline__ void cp_async(void *smem, const void *gmem) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    if (N == 16)
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
-    else
-        asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(s), "l"(gmem), "n"(N) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
 // Warp 0: exclusive scan of bcnt[0..ng) (ng <= 128) -> boff, hand out each
 // group's output range from the CTA's cursors (gbase = cur; cur += count),
@@ -551,53 +540,54 @@ __global__ void __launch_bounds__(NT, 2) k_part_refine(PartArgs pa) {
         n_b0 = b1;
         return true;
     };
-    // 16-byte copies of aligned groups of 4 rows (slot s = row - (b0 & ~3));
-    // the batch's partial first and last groups row by row (cap is a multiple of 4)
+    // TMA bulk copies of rows [b0 & ~3, round4(b1)) into buffer buf (thread 0;
+    // slot s = row - (b0 & ~3); the scratch arrays are padded so the rounded
+    // range stays inside them, and the value planes are 4-row aligned)
+    __shared__ __align__(8) uint64_t rbar[2];
     auto issue = [&](int buf, uint32_t b0, uint32_t b1) {
         unsigned char *ib = sm + buf * IN_BYTES;
-        const uint32_t base = b0 & ~3u, ng = (b1 - base + 3u) >> 2;
-        for (uint32_t gi = threadIdx.x; gi < ng; gi += NT) {
-            const uint32_t r0 = base + 4u * gi, s0 = 4u * gi;
-            if (r0 >= b0 && r0 + 4u <= b1) {
-                cp_async<16>(ib + (size_t)s0 * 4, pa.xkey + r0);
+        const uint32_t base = b0 & ~3u, nr = (b1 - base + 3u) & ~3u;
+        uint64_t *bar = &rbar[buf];
+        unsigned long long st;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 %0, [%1], %2;"
+                     : "=l"(st) : "r"((unsigned)__cvta_generic_to_shared(bar)), "r"(nr * 4u + (uint32_t)nl * nr * 8u)
+                     : "memory");
+        (void)st;
+        keys_g2s(ib, pa.xkey + base, nr * 4u, bar);
 #pragma unroll
-                for (int j = 0; j < A; ++j)
-                    if (j < nl) {
-                        unsigned char *vd = ib + (size_t)RS * 4 + ((size_t)j * RS + s0) * 8;
-                        cp_async<16>(vd, pa.xval + j * cap + r0);
-                        cp_async<16>(vd + 16, pa.xval + j * cap + r0 + 2);
-                    }
-            } else {
-                for (uint32_t u = 0; u < 4u; ++u) {
-                    const uint32_t i = r0 + u;
-                    if (i < b0 || i >= b1) continue;
-                    cp_async<4>(ib + (size_t)(s0 + u) * 4, pa.xkey + i);
-#pragma unroll
-                    for (int j = 0; j < A; ++j)
-                        if (j < nl) cp_async<8>(ib + (size_t)RS * 4 + ((size_t)j * RS + s0 + u) * 8, pa.xval + j * cap + i);
-                }
-            }
-        }
-        cp_async_commit();
+        for (int j = 0; j < A; ++j)
+            if (j < nl) keys_g2s(ib + (size_t)RS * 4 + (size_t)j * RS * 8, pa.xval + j * cap + base, nr * 8u, bar);
     };
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < 2; ++b)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((unsigned)__cvta_generic_to_shared(&rbar[b]))
+                         : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    uint32_t rphase = 0;  // parity bits of rbar[0], rbar[1]
     if (threadIdx.x < 128) bcnt[threadIdx.x] = 0u;
     uint32_t cb0 = 0, cb1 = 0, cit = 0, loaded_it = ~0u;
     bool have = next_batch(cb0, cb1, cit);
-    if (have) issue(0, cb0, cb1);
+    if (have && threadIdx.x == 0) issue(0, cb0, cb1);
     __syncthreads();
     for (int k = 0; have; ++k) {
         uint32_t nb0_ = 0, nb1_ = 0, nit_ = 0;
         const bool more = next_batch(nb0_, nb1_, nit_);
-        if (more) issue((k + 1) & 1, nb0_, nb1_);
-        else cp_async_commit();
+        if (more && threadIdx.x == 0) issue((k + 1) & 1, nb0_, nb1_);
         const uint32_t s = cit / C, tb = s * G1, ngt = min(G1, T - tb);
         if (cit != loaded_it) {  // new work item: its tiles' output cursors
             const uint32_t c = cit - s * C;
             if (threadIdx.x < ngt) cur[threadIdx.x] = pa.tstart[tb + threadIdx.x] + pa.cnt[(uint64_t)(tb + threadIdx.x) * C + c];
             loaded_it = cit;
         }
-        cp_async_wait1();
-        __syncthreads();  // (slots are filled by other threads' copies now)
+        {
+            const unsigned bar = (unsigned)__cvta_generic_to_shared(&rbar[k & 1]), par = (rphase >> (k & 1)) & 1u;
+            unsigned done = 0;
+            while (!done)
+                asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                             : "=r"(done) : "r"(bar), "r"(par) : "memory");
+            rphase ^= 1u << (k & 1);
+        }
         const unsigned char *ib = sm + (k & 1) * IN_BYTES;
         const uint32_t off = cb0 & 3u;
         uint32_t key[RPT], g[RPT], rk[RPT];

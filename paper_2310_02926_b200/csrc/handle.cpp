@@ -138,8 +138,8 @@ static int ensure_part_scratch(bin_handle *h, int64_t n, PartArgs &pa) {
     const size_t o_off1 = o; o += al((size_t)pa.T1 * (pa.C + 1) * 4);
     const size_t o_skey = o; o += al((size_t)n * 4);
     const size_t o_sval = o; o += al((size_t)capn * 8 * nv);
-    const size_t o_xkey = o; if (pa.G1 > 1) o += al((size_t)n * 4);
-    const size_t o_xval = o; if (pa.G1 > 1) o += al((size_t)capn * 8 * nv);
+    const size_t o_xkey = o; if (pa.G1 > 1) o += al(((size_t)capn + 4) * 4);     // (refine's bulk copies read whole
+    const size_t o_xval = o; if (pa.G1 > 1) o += al(((size_t)capn * nv + 4) * 8);  //  4-row groups)
     const size_t total = o;
     if (total > h->part_bytes) {
         if (h->part_base) {
